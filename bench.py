@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""Benchmark of the directional Helmholtz matvec (BASELINE.json metric:
+"directional-FMM matvec time & (N_T+N_S)/s at 1/2/4/8 B200; % FP64 roofline").
+
+A step = one apply y = A x of the configured workload (default: BASELINE config
+2, N_T = N_S = 100,000, kappa = 16, m = 4, the config the metric is quoted on
+that fits one GPU).  Setup (trees, partition, coupling matrices) is outside the
+timed region, as t_s in PAPER.md Table 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank owns a cost-balanced Morton range of target
+leaves (fdh_create_shard) and the step ends with an NCCL all-reduce of y.
+`--impl reference` times the CPU restatement of the reference algorithm
+(oracle/, OpenMP, all host cores) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2004_14229_b200.configs import CONFIGS, make_inputs  # noqa: E402
+
+METRIC = "directional-FMM matvec (N_T+N_S)/s"
+UNIT = "points/s"
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "m2l_traffic.json")
+
+
+def workload_desc(c):
+    return (f"BASELINE config {c.cfg}: N_T={c.nt}, N_S={c.ns}, kappa={c.kappa:g}, degree m={c.m} "
+            f"({(c.m + 1) ** 3} nodes/box), n_max={c.n_max}, eta2={c.eta2:g}, default directions, "
+            f"root {c.root_lo}-{c.root_hi}{', Gaussian-mixture sources' if c.mixture_sources else ''}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_oracle(c, tg, sr):
+    import oracle
+
+    return oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf, c.depth_cap,
+                         c.zero_diagonal)
+
+
+def cpu_oracle_sample(c, tg, sr, q, target_s=12.0, o=None, seed=7):
+    """The CPU restatement (oracle/) on a bounded sample: full upward pass plus
+    M2L/L2L/L2T/P2P for a seeded sample of target leaves; the full-apply time is
+    extrapolated linearly in the number of target leaves."""
+    import oracle
+
+    cores = oracle.lib().orc_set_threads(0)
+    if o is None:
+        o = build_oracle(c, tg, sr)
+    nl = o.leaf_count(0)
+    rng = np.random.default_rng(seed)
+    t = time.perf_counter()
+    o.apply_sampled(q, np.zeros(0, dtype=np.int64))
+    t0 = time.perf_counter() - t
+    k = min(nl, 16)
+    t = time.perf_counter()
+    o.apply_sampled(q, rng.choice(nl, k, replace=False))
+    tk = time.perf_counter() - t
+    per_leaf = max((tk - t0) / k, 1e-9)
+    k2 = int(min(nl, max(k, (target_s - t0) / per_leaf)))
+    t = time.perf_counter()
+    o.apply_sampled(q, rng.choice(nl, k2, replace=False))
+    tk2 = time.perf_counter() - t
+    t_full = t0 + (tk2 - t0) * nl / k2
+    return {
+        "value": (c.nt + c.ns) / t_full,
+        "unit": UNIT,
+        "cores": int(cores),
+        "kind": "port",
+        "sample": (f"oracle/ (CPU restatement, OpenMP {cores} threads): full S2M+M2M, then M2L/L2L/L2T/P2P for "
+                   f"{k2} of {nl} seeded target leaves in {tk2:.2f} s; full apply extrapolated to {t_full:.2f} s "
+                   f"(linear in target leaves; upward pass {t0:.2f} s)"),
+        "seconds_measured": tk2,
+        "apply_s_extrapolated": t_full,
+    }
+
+
+def run_reference(args, c, rank, world):
+    """--impl reference: the reference algorithm on the host cores (oracle port)."""
+    if rank != 0:
+        return
+    tg, sr, q = make_inputs(c)
+    steps = []
+    cb = None
+    o = build_oracle(c, tg, sr)
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(c, tg, sr, q, target_s=args.ref_seconds, o=o, seed=7 + i)
+        if i >= args.warmup:
+            steps.append(r["apply_s_extrapolated"])
+            cb = r
+    t = float(np.mean(steps))
+    value = (c.nt + c.ns) / t
+    cb = dict(cb)
+    cb["value"] = value
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic (seeded, SURVEY.md 8(d))",
+        "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": "cpu-openmp"},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args, c, rank, world, local_rank):
+    import torch
+
+    import paper_2004_14229_b200 as F
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    tg, sr, q = make_inputs(c)
+    t_setup = time.perf_counter()
+    op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf, c.depth_cap,
+                               c.zero_diagonal, rank=rank, world=world)
+    setup_s = time.perf_counter() - t_setup
+    st0 = op.stats()
+    stream = torch.cuda.ExternalStream(op.stream(), device=dev)
+    x = torch.from_numpy(q.view(np.float64)).to(dev)
+    y = torch.empty(2 * c.nt, dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def step():
+        op.apply_device(x.data_ptr(), y.data_ptr(), op.stream())
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    op.set_timing(True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+                evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    st = op.stats()
+    op.set_timing(False)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = args.steps * (c.nt + c.ns) / (total_ms / 1e3)
+
+    # ---- e2e: host buffers (pinned) through the C-ABI fdh_apply, copies inside
+    xh = torch.from_numpy(q.copy()).pin_memory().numpy()
+    yh = torch.empty(c.nt, dtype=torch.complex128).pin_memory().numpy()
+    for _ in range(2):
+        op.apply(xh, out=yh)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_s.record(stream)
+    for _ in range(args.steps):
+        op.apply(xh, out=yh)
+    e_e.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e_s.elapsed_time(e_e)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        dist.barrier()
+    e2e_value = args.steps * (c.nt + c.ns) / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel (M2L GEMM on FP64 DMMA)
+    peak = F.fp64_peak_tflops(0)
+    n = (c.m + 1) ** 3
+    m2l_flops = 8.0 * n * n * st["n_c"]  # algorithmic
+    gemm_ms = st["m2l_gemm_ms"]
+    achieved = m2l_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    if os.path.exists(PROFILE_TRAFFIC):
+        try:
+            tr = json.load(open(PROFILE_TRAFFIC))
+            traffic = tr.get(f"cfg{c.cfg}")
+        except Exception:
+            traffic = None
+    ph = st["phase_ms"]
+    p2p_ms = ph.get("p2p", 0.0)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "complex128 (f64)",
+        "data": "synthetic (seeded uniform / Gaussian-mixture points, U(-1,1) complex charges; SURVEY.md 8(d))",
+        "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": f"target-leaf shards x{world}",
+                   "l2": "flushed between timed steps (256 MB write, outside the step events)",
+                   "setup_s": setup_s},
+        "roofline": {"bound": "tensor", "kernel": "k_m2l_gemm (FP64 DMMA mma.sync.m8n8k4)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+                     "peak_source": "measured live: fdh_fp64_peak_tflops(0) DMMA microbenchmark (no FP64 entry in "
+                                    "MEASURED_PEAKS.json)",
+                     "algorithmic": f"8 n^2 flop per admissible block x N_C={st['n_c']} = {m2l_flops:.4g} flop per "
+                                    f"launch; executed incl. padding/empty columns {st['m2l_flops_executed']:.4g}",
+                     "gemm_ms": gemm_ms, "share_of_step": gemm_ms / ms_per_step if ms_per_step else None},
+        "phases_ms": ph,
+        "p2p": {"pairs": st["m_d"], "ms": p2p_ms,
+                "tflops_24flop_per_pair": 24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else None},
+        "counters": {k: st[k] for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s",
+                                        "depth_t", "depth_s")},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.ns, "d2h_bytes_per_step": 16 * c.nt,
+                "ms_per_step": e2e_ms / args.steps, "path": "fdh_apply (C-ABI) with pinned host buffers"},
+        "gpu_launches": int(st["gpu_launches"]) * args.steps,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = {k: v for k, v in cpu_oracle_sample(c, tg, sr, q, args.cpu_seconds).items()
+                                   if k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, never required
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+    print(json.dumps(out), flush=True)
+    del st0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        if rank == 0:
+            # bounded: at most 3 sampled steps of ~ref_seconds each
+            args.steps = min(args.steps, 2)
+            args.warmup = min(args.warmup, 1)
+            subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=False)
+        run_reference(args, c, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, c, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

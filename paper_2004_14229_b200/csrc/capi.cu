@@ -1,0 +1,524 @@
+// capi.cu -- the C-ABI (include/fdhelm_c.h): operator setup, device residency
+// and the Alg. 4 apply sequence on one CUDA stream.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fdhelm_c.h"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace fdhelm;
+
+namespace {
+thread_local std::string g_err;
+
+struct CudaErr {
+  std::string msg;
+};
+#define CK(x)                                                                                      \
+  do {                                                                                             \
+    cudaError_t e_ = (x);                                                                          \
+    if (e_ != cudaSuccess) throw CudaErr{std::string(#x) + ": " + cudaGetErrorString(e_)};         \
+  } while (0)
+
+struct LevelDev {
+  int n = 0;
+  int32_t *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr, *e = nullptr, *f = nullptr;
+  int64_t* crd = nullptr;
+};
+}  // namespace
+
+struct fdh_op {
+  Plan P;
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  Consts* dC = nullptr;
+  double* dirtab = nullptr;
+  double kappa = 0.0;
+  int64_t nt = 0, ns = 0;
+  // trees (slot order)
+  double *tx = nullptr, *ty = nullptr, *tz = nullptr, *sx = nullptr, *sy = nullptr, *sz = nullptr;
+  uint32_t *perm_t = nullptr, *perm_s = nullptr;
+  int32_t* tslot_dir = nullptr;
+  // S2M
+  int n_s2m = 0;
+  int32_t *s2m_slot = nullptr, *s2m_level = nullptr, *s2m_dir = nullptr;
+  int64_t *s2m_ci = nullptr, *s2m_cj = nullptr, *s2m_ck = nullptr;
+  uint32_t *s2m_beg = nullptr, *s2m_end = nullptr;
+  std::vector<LevelDev> m2m, l2l;
+  // L2T / P2P
+  int n_leaf = 0;
+  int32_t *l2t_level = nullptr, *l2t_slot0 = nullptr, *l2t_nslot = nullptr;
+  int64_t *l2t_ci = nullptr, *l2t_cj = nullptr, *l2t_ck = nullptr;
+  uint32_t *l2t_beg = nullptr, *l2t_end = nullptr;
+  int64_t* p2p_ptr = nullptr;
+  uint32_t *p2p_sbeg = nullptr, *p2p_send = nullptr;
+  // M2L
+  int n_item = 0, n_tile = 0;
+  int32_t *item_tile = nullptr, *tile_keys = nullptr, *tile_src = nullptr, *tile_item0 = nullptr,
+          *tile_nitem = nullptr, *tile_tslot = nullptr;
+  int64_t *item_k0 = nullptr, *item_k1 = nullptr;
+  int32_t *key_level = nullptr, *key_dir = nullptr;
+  int64_t* key_d = nullptr;
+  double *W = nullptr, *mom = nullptr, *loc = nullptr, *partial = nullptr;
+  double2 *q = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
+  int* flag = nullptr;
+  bool timing = false;
+  static constexpr int kRing = 64;
+  cudaEvent_t ring[kRing][FDH_NPHASES + 3] = {};  // phase boundaries + M2L GEMM start/stop
+  int ring_n = 0;                                 // applies recorded since the last reset
+  cudaEvent_t ev[FDH_NPHASES + 1] = {};
+  cudaEvent_t ev_all[2] = {};
+  fdh_stats stats{};
+  int64_t launches = 0;
+  bool applied = false;
+  int rank = 0, world = 1;
+
+  ~fdh_op() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : allocs) cudaFree(p);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_all)
+      if (e) cudaEventDestroy(e);
+    for (auto& r : ring)
+      for (auto& e : r)
+        if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    if (count == 0) return nullptr;
+    void* p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess)
+      throw CudaErr{"cudaMalloc(" + std::to_string(count * sizeof(T)) + " B): " + cudaGetErrorString(e)};
+    allocs.push_back(p);
+    bytes += (int64_t)(count * sizeof(T));
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* up(const std::vector<T>& v) {
+    if (v.empty()) return nullptr;
+    T* d = alloc<T>(v.size());
+    CK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+};
+
+namespace {
+
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+
+void setup_device(fdh_op* o) {
+  Plan& P = o->P;
+  CK(cudaGetDevice(&o->device));
+  CK(cudaStreamCreateWithFlags(&o->st, cudaStreamNonBlocking));
+  for (auto& e : o->ev) CK(cudaEventCreate(&e));
+  for (auto& e : o->ev_all) CK(cudaEventCreate(&e));
+  for (auto& r : o->ring)
+    for (auto& e : r) CK(cudaEventCreate(&e));
+  // constants
+  Consts C{};
+  C.kappa = P.prm.kappa;
+  C.m = P.prm.m;
+  C.p = P.p;
+  C.n = P.n;
+  C.n_pad = P.n_pad;
+  C.lhf = P.lhf;
+  C.zero_diag = P.prm.zero_diagonal;
+  for (int i = 0; i < P.p; ++i) C.cheb_cos[i] = P.cheb_cos[i];
+  for (int h = 0; h < 2; ++h)
+    for (int j = 0; j < P.p; ++j)
+      for (int k = 0; k < P.p; ++k) C.half[(h * P.p + j) * P.p + k] = P.half[(h * P.p + j) * P.p + k];
+  for (int a = 0; a < 3; ++a) {
+    C.lo_t[a] = P.T.lo[a];
+    C.lo_s[a] = P.S.lo[a];
+  }
+  if (P.T.depth >= kMaxLevels - 1 || P.S.depth >= kMaxLevels - 1) throw PlanError{4, "tree too deep"};
+  for (int l = 0; l <= P.T.depth; ++l)
+    for (int a = 0; a < 3; ++a) C.side_t[l][a] = P.T.side[l][a];
+  for (int l = 0; l <= P.S.depth; ++l)
+    for (int a = 0; a < 3; ++a) C.side_s[l][a] = P.S.side[l][a];
+  std::vector<double> dt;
+  for (int l = 0; l < (int)P.dirvec.size(); ++l) {
+    C.dir_off[l] = (int)dt.size();
+    dt.insert(dt.end(), P.dirvec[l].begin(), P.dirvec[l].end());
+  }
+  C.dir_off[P.dirvec.size()] = (int)dt.size();
+  o->dC = o->alloc<Consts>(1);
+  CK(cudaMemcpy(o->dC, &C, sizeof(C), cudaMemcpyHostToDevice));
+  o->dirtab = o->up(dt);
+  o->kappa = P.prm.kappa;
+  // trees
+  o->nt = (int64_t)P.T.perm.size();
+  o->ns = (int64_t)P.S.perm.size();
+  o->tx = o->up(P.T.x);
+  o->ty = o->up(P.T.y);
+  o->tz = o->up(P.T.z);
+  o->sx = o->up(P.S.x);
+  o->sy = o->up(P.S.y);
+  o->sz = o->up(P.S.z);
+  o->perm_t = o->up(P.T.perm);
+  o->perm_s = o->up(P.S.perm);
+  o->tslot_dir = o->up(P.T.slot_dir);
+  // S2M
+  o->n_s2m = (int)P.s2m_slot.size();
+  o->s2m_slot = o->up(P.s2m_slot);
+  o->s2m_level = o->up(P.s2m_level);
+  o->s2m_dir = o->up(P.s2m_dir);
+  o->s2m_ci = o->up(P.s2m_ci);
+  o->s2m_cj = o->up(P.s2m_cj);
+  o->s2m_ck = o->up(P.s2m_ck);
+  o->s2m_beg = o->up(P.s2m_begin);
+  o->s2m_end = o->up(P.s2m_end);
+  // M2M / L2L per level
+  o->m2m.assign(P.m2m_parent.size(), {});
+  for (size_t l = 0; l < P.m2m_parent.size(); ++l) {
+    LevelDev& D = o->m2m[l];
+    D.n = (int)P.m2m_parent[l].size();
+    D.a = o->up(P.m2m_parent[l]);
+    D.b = o->up(P.m2m_dir[l]);
+    D.c = o->up(P.m2m_cdir[l]);
+    D.d = o->up(P.m2m_child[l]);
+    D.crd = o->up(P.m2m_pc[l]);
+  }
+  o->l2l.assign(P.l2l_child.size(), {});
+  for (size_t l = 0; l < P.l2l_child.size(); ++l) {
+    LevelDev& D = o->l2l[l];
+    D.n = (int)P.l2l_child[l].size();
+    D.a = o->up(P.l2l_child[l]);
+    D.b = o->up(P.l2l_cdir[l]);
+    D.c = o->up(P.l2l_ptr[l]);
+    D.d = o->up(P.l2l_pslot[l]);
+    D.e = o->up(P.l2l_pdir[l]);
+    D.f = o->up(P.l2l_oct[l]);
+    D.crd = o->up(P.l2l_cc[l]);
+  }
+  // L2T / P2P
+  o->n_leaf = (int)P.l2t_level.size();
+  o->l2t_level = o->up(P.l2t_level);
+  o->l2t_slot0 = o->up(P.l2t_slot0);
+  o->l2t_nslot = o->up(P.l2t_nslot);
+  o->l2t_ci = o->up(P.l2t_ci);
+  o->l2t_cj = o->up(P.l2t_cj);
+  o->l2t_ck = o->up(P.l2t_ck);
+  o->l2t_beg = o->up(P.l2t_begin);
+  o->l2t_end = o->up(P.l2t_end);
+  o->p2p_ptr = o->up(P.p2p_ptr);
+  o->p2p_sbeg = o->up(P.p2p_sbeg);
+  o->p2p_send = o->up(P.p2p_send);
+  // M2L
+  o->n_item = (int)P.item_tile.size();
+  o->n_tile = (int)P.tile_level.size();
+  o->item_tile = o->up(P.item_tile);
+  o->item_k0 = o->up(P.item_k0);
+  o->item_k1 = o->up(P.item_k1);
+  o->tile_keys = o->up(P.tile_keys);
+  o->tile_src = o->up(P.tile_src);
+  o->tile_item0 = o->up(P.tile_item0);
+  o->tile_nitem = o->up(P.tile_nitem);
+  o->tile_tslot = o->up(P.tile_tslot);
+  o->key_level = o->up(P.key_level);
+  o->key_dir = o->up(P.key_dir);
+  {
+    std::vector<int64_t> kd(3 * P.key_level.size());
+    for (size_t k = 0; k < P.key_level.size(); ++k) {
+      kd[3 * k] = P.key_dx[k];
+      kd[3 * k + 1] = P.key_dy[k];
+      kd[3 * k + 2] = P.key_dz[k];
+    }
+    o->key_d = o->up(kd);
+  }
+  const int64_t np2 = 2 * (int64_t)P.n_pad;
+  const int64_t nkeys = (int64_t)P.key_level.size();
+  o->W = o->alloc<double>((size_t)(nkeys * P.n_pad * np2));
+  o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
+  o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
+  o->partial = o->alloc<double>((size_t)((int64_t)o->n_item * P.n_pad * 2 * P.prm.tile));
+  o->q = o->alloc<double2>((size_t)o->ns);
+  o->yslot = o->alloc<double2>((size_t)o->nt);
+  o->xin = o->alloc<double2>((size_t)o->ns);
+  o->yout = o->alloc<double2>((size_t)o->nt);
+  o->flag = o->alloc<int>(1);
+  // coupling matrices (populated at setup), in key chunks
+  const int64_t chunk = 4096;
+  for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+    launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
+                    o->W, P.n, P.n_pad);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(o->st));
+  if (o->n_item > 0 && (P.n_pad != 32 && P.n_pad != 64 && P.n_pad != 128 && P.n_pad != 224 && P.n_pad != 352))
+    throw PlanError{4, "interpolation degree m=" + std::to_string(P.prm.m) + " has no compiled M2L kernel"};
+}
+
+void rec(fdh_op* o, int ph, cudaStream_t st) {
+  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][ph], st));
+}
+
+// Alg. 4 on the device: x_dev (original order) -> y_dev (original order).
+void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
+  Plan& P = o->P;
+  const int n = P.n, np = P.n_pad;
+  int64_t L = 0;
+  CK(cudaEventRecord(o->ev_all[0], st));
+  rec(o, FDH_PHASE_H2D, st);
+  CK(cudaMemsetAsync(o->flag, 0, sizeof(int), st));
+  launch_gather_charges(st, o->ns, o->perm_s, x, o->q);
+  ++L;
+  rec(o, FDH_PHASE_S2M, st);
+  launch_s2m(st, o->dC, o->dirtab, o->n_s2m, o->s2m_slot, o->s2m_level, o->s2m_dir, o->s2m_ci, o->s2m_cj, o->s2m_ck,
+             o->s2m_beg, o->s2m_end, o->sx, o->sy, o->sz, o->q, o->mom, n, np);
+  L += o->n_s2m > 0;
+  rec(o, FDH_PHASE_M2M, st);
+  for (int l = (int)o->m2m.size() - 1; l >= 0; --l) {
+    const LevelDev& D = o->m2m[l];
+    if (D.n == 0) continue;
+    launch_m2m(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.c, D.d, D.crd, o->mom, n, np);
+    ++L;
+  }
+  rec(o, FDH_PHASE_M2L, st);
+  CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(P.T.nslots * 2 * np), st));
+  if (o->n_item > 0) {
+    rec(o, FDH_NPHASES + 1, st);
+    if (launch_m2l_gemm(st, np, P.prm.tile, o->n_item, o->item_tile, o->item_k0, o->item_k1, o->tile_keys,
+                        o->tile_src, o->W, o->mom, o->partial) != 0)
+      throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+    rec(o, FDH_NPHASES + 2, st);
+    launch_m2l_reduce(st, np, P.prm.tile, o->n_tile, o->tile_item0, o->tile_nitem, o->tile_tslot, o->partial,
+                      o->loc);
+    L += 2;
+  }
+  rec(o, FDH_PHASE_L2L, st);
+  for (int l = 0; l < (int)o->l2l.size(); ++l) {
+    const LevelDev& D = o->l2l[l];
+    if (D.n == 0) continue;
+    launch_l2l(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.crd, D.c, D.d, D.e, D.f, o->loc, n, np);
+    ++L;
+  }
+  rec(o, FDH_PHASE_L2T, st);
+  if (o->world > 1) CK(cudaMemsetAsync(o->yslot, 0, sizeof(double2) * (size_t)o->nt, st));
+  launch_l2t(st, o->dC, o->dirtab, o->n_leaf, o->l2t_level, o->l2t_slot0, o->l2t_nslot, o->l2t_ci, o->l2t_cj,
+             o->l2t_ck, o->l2t_beg, o->l2t_end, o->tx, o->ty, o->tz, o->tslot_dir, o->loc, o->yslot, n, np);
+  L += o->n_leaf > 0;
+  rec(o, FDH_PHASE_P2P, st);
+  launch_p2p(st, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
+             o->tz, o->sx, o->sy, o->sz, o->q, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->yslot, o->flag);
+  L += o->n_leaf > 0;
+  rec(o, FDH_PHASE_D2H, st);
+  launch_scatter_y(st, o->nt, o->perm_t, o->yslot, y);
+  ++L;
+  rec(o, FDH_NPHASES, st);
+  CK(cudaEventRecord(o->ev_all[1], st));
+  CK(cudaGetLastError());
+  o->launches = L;
+  o->applied = true;
+  if (o->timing) ++o->ring_n;
+}
+
+void collect_times(fdh_op* o) {
+  if (!o->applied) return;
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, o->ev_all[0], o->ev_all[1]));
+  o->stats.apply_ms = ms;
+  // per-phase averages over the applies recorded since the last fdh_set_timing
+  const int nr = std::min(o->ring_n, fdh_op::kRing);
+  if (nr > 0) {
+    double acc[FDH_NPHASES + 1] = {0};
+    for (int r = 0; r < nr; ++r) {
+      for (int ph = 0; ph < FDH_NPHASES; ++ph) {
+        CK(cudaEventElapsedTime(&ms, o->ring[r][ph], o->ring[r][ph + 1]));
+        acc[ph] += ms;
+      }
+      if (o->n_item > 0) {
+        CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 1], o->ring[r][FDH_NPHASES + 2]));
+        acc[FDH_NPHASES] += ms;
+      }
+    }
+    for (int ph = 0; ph < FDH_NPHASES; ++ph) o->stats.phase_ms[ph] = acc[ph] / nr;
+    o->stats.m2l_gemm_ms = acc[FDH_NPHASES] / nr;
+    o->stats.timed_applies = nr;
+  }
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FDH_OK;
+  } catch (const PlanError& e) {
+    return fail(e.code, e.msg);
+  } catch (const CudaErr& e) {
+    return fail(FDH_ERR_CUDA, e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(FDH_ERR_MEMORY, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(FDH_ERR_ARG, e.what());
+  }
+}
+
+int create_common(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                  const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
+                  double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
+                  int world, fdh_op** out, bool device = true) {
+  if (!out) return fail(FDH_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (!tx || !ty || !tz || !sx || !sy || !sz || !lo || !hi) return fail(FDH_ERR_ARG, "NULL input pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(FDH_ERR_ARG, "invalid rank / world");
+  int ndev = 0;
+  if (device && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0))
+    return fail(FDH_ERR_CUDA, "no CUDA device available");
+  fdh_op* o = new fdh_op;
+  const int rc = guard([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    PlanParams prm;
+    prm.kappa = kappa;
+    prm.n_max = n_max;
+    prm.m = m;
+    prm.eta2 = eta2;
+    prm.l_hf = l_hf;
+    prm.depth_cap = depth_cap;
+    prm.zero_diagonal = zero_diagonal;
+    prm.rank = rank;
+    prm.world = world;
+    o->rank = rank;
+    o->world = world;
+    build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
+    if (device) setup_device(o);
+    o->stats.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  });
+  if (rc != FDH_OK) {
+    delete o;
+    return rc;
+  }
+  *out = o;
+  return FDH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fdh_last_error(void) { return g_err.c_str(); }
+const char* fdh_version(void) { return "fdhelm-b200 0.1 (sm_100a, FP64 DMMA M2L)"; }
+
+int fdh_create(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx, const double* sy,
+               const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3], double kappa, int n_max,
+               int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int n_gpus, fdh_op** out) {
+  if (n_gpus != 1)
+    return fail(FDH_ERR_UNSUPPORTED, "n_gpus must be 1: run one operator per rank via fdh_create_shard");
+  return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
+                       zero_diagonal, 0, 1, out);
+}
+
+int fdh_create_shard(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                     const double* sy, const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3],
+                     double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
+                     int world, fdh_op** out) {
+  return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
+                       zero_diagonal, rank, world, out);
+}
+
+int fdh_plan_only(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx, const double* sy,
+                  const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3], double kappa,
+                  int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank, int world,
+                  fdh_op** out) {
+  return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
+                       zero_diagonal, rank, world, out, false);
+}
+
+void fdh_destroy(fdh_op* op) { delete op; }
+
+int fdh_apply(fdh_op* o, const double* x, double* y) {
+  if (!o || !x || !y) return fail(FDH_ERR_ARG, "NULL argument");
+  if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
+  return guard([&] {
+    CK(cudaSetDevice(o->device));
+    CK(cudaMemcpyAsync(o->xin, x, sizeof(double2) * (size_t)o->ns, cudaMemcpyHostToDevice, o->st));
+    apply_device(o, o->xin, o->yout, o->st);
+    CK(cudaMemcpyAsync(y, o->yout, sizeof(double2) * (size_t)o->nt, cudaMemcpyDeviceToHost, o->st));
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost, o->st));
+    CK(cudaStreamSynchronize(o->st));
+    collect_times(o);
+    if (flag) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+  });
+}
+
+int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream) {
+  if (!o || !x_dev || !y_dev) return fail(FDH_ERR_ARG, "NULL argument");
+  if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
+  return guard([&] {
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : o->st;
+    apply_device(o, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), st);
+  });
+}
+
+void* fdh_stream(fdh_op* o) { return o ? static_cast<void*>(o->st) : nullptr; }
+
+int fdh_set_timing(fdh_op* o, int enable) {
+  if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  o->timing = enable != 0;
+  o->ring_n = 0;
+  return FDH_OK;
+}
+
+int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
+  if (!o || !s) return fail(FDH_ERR_ARG, "NULL argument");
+  fdh_op* m = const_cast<fdh_op*>(o);
+  if (m->st) {
+    cudaStreamSynchronize(m->st);
+    try {
+      collect_times(m);
+    } catch (...) {
+    }
+  }
+  const Plan& P = o->P;
+  *s = o->stats;
+  s->n_le = P.n_le;
+  s->n_c = P.n_c;
+  s->n_sc = P.n_sc;
+  s->m_d = P.m_d;
+  s->n_lminus = P.n_lminus;
+  s->nf_percent = 100.0 * (double)P.m_d / ((double)o->nt * (double)o->ns);
+  s->bytes_stored = o->bytes;
+  s->depth_t = P.T.depth;
+  s->depth_s = P.S.depth;
+  s->l_hf = P.lhf;
+  s->n_pad = P.n_pad;
+  s->slots_t = P.T.nslots;
+  s->slots_s = P.S.nslots;
+  int64_t nn = 0;
+  for (auto& L : P.T.lv) nn += (int64_t)L.size();
+  s->nodes_t = nn;
+  nn = 0;
+  for (auto& L : P.S.lv) nn += (int64_t)L.size();
+  s->nodes_s = nn;
+  s->gpu_launches = o->launches;
+  s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;
+  return FDH_OK;
+}
+
+int64_t fdh_export_tree(const fdh_op* o, int which, int64_t* rows) {
+  return o ? export_tree(which == 0 ? o->P.T : o->P.S, rows) : -1;
+}
+int64_t fdh_export_perm(const fdh_op* o, int which, int64_t* perm) {
+  return o ? export_perm(which == 0 ? o->P.T : o->P.S, perm) : -1;
+}
+int64_t fdh_export_lplus(const fdh_op* o, int64_t* rows) { return o ? export_lplus(o->P, rows) : -1; }
+int64_t fdh_export_lminus(const fdh_op* o, int64_t* rows) { return o ? export_lminus(o->P, rows) : -1; }
+int64_t fdh_export_dirsets(const fdh_op* o, int which, int64_t* rows) {
+  return o ? export_dirsets(o->P, which, rows) : -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,273 @@
+// k_m2l.cu -- coupling matrices and the M2L phase on FP64 DMMA (sm_100a).
+//
+// M2L: g~_{t,c} += A_{c,t x s} v~_{s,c} for every admissible
+// leaf (t,s).  A depends only on the key (level, lattice offset) (PAPER.md:397-399,
+// SPEC.md:422-439), so the pairs of a TILE of target slots (same level, direction
+// and lattice parity -> nearly identical key lists) form, per key, a real GEMM
+//
+//     C[n_pad x 2T] += W_key[n_pad x 2 n_pad] * B[2 n_pad x 2T]
+//     W = [Re A | Im A],  B(:,2j) = [Re v_j ; -Im v_j],  B(:,2j+1) = [Im v_j ; Re v_j]
+//
+// so that C(:,2j) = Re(A v_j) and C(:,2j+1) = Im(A v_j): the complex product is a
+// single real GEMM with 8 n^2 flops per block.  It runs on
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), the only FP64 tensor-core path on
+// sm_100a (tcgen05 has no f64 kind).  Each warp owns 32 rows x 2T columns in
+// registers; A fragments stream from L2 straight into registers (no reuse
+// across warps), the gathered moments are staged once per key in shared
+// memory (cp.async, double-buffered) and shared by all warps.  Split-K over the
+// key list gives work items; partial sums are reduced in a fixed order
+// (deterministic, no atomics).
+#include "kernels.hpp"
+
+namespace fdhelm {
+
+namespace {
+
+constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // geometry.hpp:11
+
+// ---------------------------------------------------------- coupling gen
+// W[key][j][k] = Re f_c(xi_t,j, xi_s,k),  W[key][j][n_pad + k] = Im f_c(...)
+// canonical frame: s at the lattice origin, t at offset d.
+constexpr int kCplRows = 8;
+__global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, const double* __restrict__ dirtab,
+                                                  int64_t key0, const int32_t* __restrict__ key_level,
+                                                  const int64_t* __restrict__ key_d, const int32_t* __restrict__ key_dir,
+                                                  double* __restrict__ W, int n, int n_pad) {
+  __shared__ double tn[3][kMaxP], sn[3][kMaxP];
+  const int64_t key = key0 + blockIdx.x;
+  const int r0 = blockIdx.y * kCplRows;
+  const int p = C->p;
+  const int l = key_level[key];
+  if (threadIdx.x < 3 * p) {
+    const int a = threadIdx.x / p, nu = threadIdx.x % p;
+    const double side = C->side_t[l][a];
+    const int64_t d = key_d[3 * key + a];
+    tn[a][nu] = cheb_node(__dmul_rn((double)d, side), __dmul_rn((double)(d + 1), side), C->cheb_cos[nu]);
+    sn[a][nu] = cheb_node(0.0, __dmul_rn(1.0, side), C->cheb_cos[nu]);
+  }
+  const double* c = dir_vec(C, dirtab, l, key_dir[key]);
+  const double cv[3] = {c[0], c[1], c[2]};
+  const double kappa = C->kappa;
+  __syncthreads();
+  double* Wk = W + key * n_pad * 2 * n_pad;
+  for (int idx = threadIdx.x; idx < kCplRows * n_pad; idx += blockDim.x) {
+    const int j = r0 + idx / n_pad, k = idx % n_pad;
+    if (j >= n_pad) continue;
+    double re = 0.0, im = 0.0;
+    if (j < n && k < n) {
+      const double d[3] = {__dsub_rn(tn[0][j / (p * p)], sn[0][k / (p * p)]),
+                           __dsub_rn(tn[1][(j / p) % p], sn[1][(k / p) % p]),
+                           __dsub_rn(tn[2][j % p], sn[2][k % p])};
+      const double r = sqrt(dot3(d, d));  // geometry.hpp:92-98
+      const double ph = __dmul_rn(kappa, __dsub_rn(r, dot3(d, cv)));
+      const double w = __ddiv_rn(1.0, __dmul_rn(kFourPi, r));
+      double s, co;
+      sincos(ph, &s, &co);
+      re = __dmul_rn(w, co);
+      im = __dmul_rn(w, s);
+    }
+    Wk[(int64_t)j * 2 * n_pad + k] = re;
+    Wk[(int64_t)j * 2 * n_pad + n_pad + k] = im;
+  }
+}
+
+// ---------------------------------------------------------------- DMMA
+__device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int NPAD, int TT>
+struct M2LShape {
+  static constexpr int K2 = 2 * NPAD;       // GEMM K (and W row length)
+  static constexpr int MS = 2 * NPAD + 8;   // smem moment stride (bank spread)
+  static constexpr int IMOFF = NPAD + 4;    // smem offset of the imaginary plane
+  static constexpr int NT = 2 * TT / 8;     // 8-column n-tiles per warp
+  static constexpr int THREADS = NPAD;      // one warp per 32 rows
+  static constexpr int STAGE = TT * MS;     // doubles per smem stage
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(double);
+};
+
+template <int NPAD, int TT>
+__device__ __forceinline__ void m2l_stage(double* buf, const int32_t* __restrict__ src, const double* __restrict__ mom) {
+  using S = M2LShape<NPAD, TT>;
+  // TT columns x NPAD 16-byte chunks (first NPAD/2 chunks: re plane, then im plane)
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < TT * NPAD; idx += S::THREADS) {
+    const int c = idx / NPAD, ch = idx % NPAD;
+    const int32_t s = src[c];
+    double* dst = buf + c * S::MS + (ch < NPAD / 2 ? 2 * ch : S::IMOFF + 2 * (ch - NPAD / 2));
+    if (s >= 0) {
+      cp_async16(dst, mom + (int64_t)s * S::K2 + 2 * ch);
+    } else {
+      dst[0] = 0.0;
+      dst[1] = 0.0;
+    }
+  }
+}
+
+template <int NPAD, int TT>
+__global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ item_tile,
+                                                   const int64_t* __restrict__ item_k0,
+                                                   const int64_t* __restrict__ item_k1,
+                                                   const int32_t* __restrict__ tile_keys,
+                                                   const int32_t* __restrict__ tile_src,
+                                                   const double* __restrict__ W, const double* __restrict__ mom,
+                                                   double* __restrict__ partial) {
+  using S = M2LShape<NPAD, TT>;
+  constexpr int NT = S::NT;
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  const int64_t k0 = item_k0[item], k1 = item_k1[item];
+  (void)item_tile;
+
+  double acc[4][NT][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // B fragment addressing: lane holds B[k0 + (lane&3)][nt*8 + lane/4]
+  //   column col = nt*8 + lane/4 -> source c = nt*4 + lane/8, parity = (lane>>2)&1
+  const int bpar = (lane >> 2) & 1;
+  const int bcol = lane >> 3;
+  const int bk = lane & 3;
+  const int re_off = bpar ? S::IMOFF : 0;   // first K half: parity 0 -> Re, 1 -> Im
+  const int im_off = bpar ? 0 : S::IMOFF;   // second K half: parity 0 -> -Im, 1 -> Re
+  const double sgn = bpar ? 1.0 : -1.0;
+
+  m2l_stage<NPAD, TT>(smem, tile_src + k0 * TT, mom);
+  cp_async_commit();
+  int stage = 0;
+  for (int64_t kk = k0; kk < k1; ++kk) {
+    if (kk + 1 < k1) m2l_stage<NPAD, TT>(smem + (stage ^ 1) * S::STAGE, tile_src + (kk + 1) * TT, mom);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* __restrict__ Wk =
+        W + (int64_t)tile_keys[kk] * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
+    const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
+    // K half 1: columns of Re A against (Re v, Im v)
+#pragma unroll 4
+    for (int ks = 0; ks < NPAD / 4; ++ks) {
+      double a[4], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + mt * 8 * S::K2 + 4 * ks);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = Bs[nt * 4 * S::MS + re_off + 4 * ks];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+    }
+    // K half 2: columns of Im A against (-Im v, Re v)
+#pragma unroll 4
+    for (int ks = 0; ks < NPAD / 4; ++ks) {
+      double a[4], b[NT];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + NPAD + mt * 8 * S::K2 + 4 * ks);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = sgn * Bs[nt * 4 * S::MS + im_off + 4 * ks];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+    }
+    __syncthreads();
+    stage ^= 1;
+  }
+  double* P = partial + (int64_t)item * NPAD * 2 * TT;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int row = warp * 32 + mt * 8 + (lane >> 2);
+      const int col = nt * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(P + (int64_t)row * 2 * TT + col) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    }
+}
+
+// Sum the partials of each tile's work items in item order and store the
+// locals of its target slots (planar re | im).
+template <int NPAD, int TT>
+__global__ void __launch_bounds__(256) k_m2l_reduce(const int32_t* __restrict__ tile_item0,
+                                                    const int32_t* __restrict__ tile_nitem,
+                                                    const int32_t* __restrict__ tile_tslot,
+                                                    const double* __restrict__ partial, double* __restrict__ loc) {
+  const int tile = blockIdx.x;
+  const int i0 = tile_item0[tile], ni = tile_nitem[tile];
+  for (int idx = threadIdx.x; idx < NPAD * 2 * TT; idx += blockDim.x) {
+    const int row = idx / (2 * TT), col = idx % (2 * TT);
+    const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
+    if (ts < 0) continue;
+    double s = 0.0;
+    for (int i = 0; i < ni; ++i) s += partial[(int64_t)(i0 + i) * NPAD * 2 * TT + idx];
+    loc[(int64_t)ts * 2 * NPAD + ((col & 1) ? NPAD : 0) + row] = s;
+  }
+}
+
+template <int NPAD, int TT>
+void run_gemm(cudaStream_t st, int n_item, const int32_t* item_tile, const int64_t* item_k0, const int64_t* item_k1,
+              const int32_t* tile_keys, const int32_t* tile_src, const double* W, const double* mom,
+              double* partial) {
+  using S = M2LShape<NPAD, TT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_m2l_gemm<NPAD, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+    attr = true;
+  }
+  k_m2l_gemm<NPAD, TT><<<n_item, S::THREADS, S::SMEM, st>>>(item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom,
+                                                            partial);
+}
+
+}  // namespace
+
+void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
+                     const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double* W, int n,
+                     int n_pad) {
+  if (nkeys <= 0) return;
+  dim3 grid((unsigned)nkeys, (unsigned)((n_pad + kCplRows - 1) / kCplRows));
+  k_coupling<<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, W, n, n_pad);
+}
+
+int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int32_t* item_tile,
+                    const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
+                    const int32_t* tile_src, const double* W, const double* mom, double* partial) {
+  if (n_item <= 0) return 0;
+  if (tile != 16) return 1;
+  switch (n_pad) {
+    case 32: run_gemm<32, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    case 64: run_gemm<64, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    case 128: run_gemm<128, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    case 224: run_gemm<224, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    case 352: run_gemm<352, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    default: return 1;
+  }
+  return 0;
+}
+
+void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_item0,
+                       const int32_t* tile_nitem, const int32_t* tile_tslot, const double* partial, double* loc) {
+  if (n_tile <= 0 || tile != 16) return;
+  switch (n_pad) {
+    case 32: k_m2l_reduce<32, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    case 64: k_m2l_reduce<64, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    case 128: k_m2l_reduce<128, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    case 224: k_m2l_reduce<224, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    case 352: k_m2l_reduce<352, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    default: break;
+  }
+}
+
+}  // namespace fdhelm

@@ -1,0 +1,46 @@
+// kernels.hpp -- host-side launchers of the apply kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace fdhelm {
+
+// ---- k_apply.cu
+void launch_gather_charges(cudaStream_t st, int64_t ns, const uint32_t* perm, const double2* x, double2* q);
+void launch_scatter_y(cudaStream_t st, int64_t nt, const uint32_t* perm, const double2* y_slot, double2* y);
+void launch_s2m(cudaStream_t st, const Consts* C, const double* dirtab, int n_entry, const int32_t* slot,
+                const int32_t* level, const int32_t* dir, const int64_t* ci, const int64_t* cj, const int64_t* ck,
+                const uint32_t* beg, const uint32_t* end, const double* px, const double* py, const double* pz,
+                const double2* q, double* mom, int n, int n_pad);
+void launch_m2m(cudaStream_t st, const Consts* C, const double* dirtab, int level, int n_entry,
+                const int32_t* parent, const int32_t* pdir, const int32_t* cdir, const int32_t* child,
+                const int64_t* pc, double* mom, int n, int n_pad);
+void launch_l2l(cudaStream_t st, const Consts* C, const double* dirtab, int level, int n_entry,
+                const int32_t* child, const int32_t* cdir, const int64_t* cc, const int32_t* ptr,
+                const int32_t* pslot, const int32_t* pdir, const int32_t* oct, double* loc, int n, int n_pad);
+void launch_l2t(cudaStream_t st, const Consts* C, const double* dirtab, int n_entry, const int32_t* level,
+                const int32_t* slot0, const int32_t* nslot, const int64_t* ci, const int64_t* cj,
+                const int64_t* ck, const uint32_t* beg, const uint32_t* end, const double* px,
+                const double* py, const double* pz, const int32_t* slot_dir, const double* loc,
+                double2* y_slot, int n, int n_pad);
+void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg, const uint32_t* end,
+                const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
+                const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
+                const double2* q, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
+                double2* y_slot, int* flag);
+
+// ---- k_m2l.cu
+void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
+                     const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double* W,
+                     int n, int n_pad);
+// returns 0 on success, nonzero if n_pad / tile combination is not compiled
+int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int32_t* item_tile,
+                    const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
+                    const int32_t* tile_src, const double* W, const double* mom, double* partial);
+void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_item0,
+                       const int32_t* tile_nitem, const int32_t* tile_tslot, const double* partial,
+                       double* loc);
+
+}  // namespace fdhelm

@@ -1,0 +1,865 @@
+// plan.cpp -- level-synchronous setup of the directional matvec (see plan.hpp).
+//
+// Compiled with -ffp-contract=off: the octant and admissibility decisions must
+// use the reference's separate FP64 multiply and add (cluster_tree.cpp:73-77,
+// geometry.hpp:69-76) to be bit-exact with it.
+#include "plan.hpp"
+
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <unordered_map>
+
+namespace fdhelm {
+
+namespace {
+constexpr double kRootPad = 1e-12;  // cluster_tree.cpp:9
+constexpr double kPi = 3.141592653589793;
+
+[[noreturn]] void fail(int code, const std::string& m) { throw PlanError{code, m}; }
+
+inline double norm3(const double* a) { return std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+// PAPER.md Alg. 1 (cluster_tree.cpp:12-128), level by level: every node of a
+// level that holds more than n_max points (and is below the depth cap) is
+// split by the stable octant partition; ranges of distinct nodes are disjoint,
+// so the nodes of one level are partitioned in parallel.
+void build_tree(TreePlan& T, const double* x, const double* y, const double* z, int64_t n, const double lo[3],
+                const double hi[3], int nmax, int cap) {
+  if (n <= 0) fail(1, "cluster tree: empty point set");
+  if (nmax < 1) fail(1, "cluster tree: n_max must be >= 1");
+  if (!(lo[0] < hi[0] && lo[1] < hi[1] && lo[2] < hi[2])) fail(1, "cluster tree: invalid root box");
+  if (n > (int64_t)UINT32_MAX) fail(4, "cluster tree: more than 2^32-1 points");
+  for (int a = 0; a < 3; ++a) {
+    T.lo[a] = lo[a] - kRootPad * (hi[a] - lo[a]);
+    T.hi[a] = hi[a];
+  }
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
+  for (int64_t i = 0; i < n; ++i) {
+    const bool in = x[i] > T.lo[0] && x[i] <= T.hi[0] && y[i] > T.lo[1] && y[i] <= T.hi[1] && z[i] > T.lo[2] &&
+                    z[i] <= T.hi[2];
+    if (!in) bad = 1;
+  }
+  if (bad) fail(1, "cluster tree: point outside root box");
+  T.x.assign(x, x + n);
+  T.y.assign(y, y + n);
+  T.z.assign(z, z + n);
+  T.perm.resize(n);
+  for (int64_t i = 0; i < n; ++i) T.perm[i] = (uint32_t)i;
+  T.side.push_back({T.hi[0] - T.lo[0], T.hi[1] - T.lo[1], T.hi[2] - T.lo[2]});
+  T.diam.push_back(norm3(T.side[0].data()));
+  T.lv.emplace_back();
+  {
+    LevelNodes& L0 = T.lv[0];
+    L0.ci = {0}; L0.cj = {0}; L0.ck = {0};
+    L0.begin = {0}; L0.end = {(uint32_t)n};
+    L0.leaf = {1}; L0.parent = {-1};
+  }
+  T.oversized = 0;
+  for (int l = 0;; ++l) {
+    LevelNodes& L = T.lv[l];
+    const size_t nn = L.size();
+    L.child.assign(nn * 8, -1);
+    std::vector<int32_t> refine;
+    for (size_t i = 0; i < nn; ++i) {
+      const uint32_t cnt = L.end[i] - L.begin[i];
+      if (cnt <= (uint32_t)nmax) continue;
+      if (l >= cap) { ++T.oversized; continue; }
+      refine.push_back((int32_t)i);
+    }
+    if (refine.empty()) { T.depth = l; break; }
+    if (l + 1 > 21) fail(4, "cluster tree deeper than 21 levels is not supported by this build");
+    const auto& s = T.side[l];
+    T.side.push_back({0.5 * s[0], 0.5 * s[1], 0.5 * s[2]});
+    T.diam.push_back(norm3(T.side[l + 1].data()));
+    const auto cs = T.side[l + 1];
+    std::vector<std::array<uint32_t, 8>> cnt(refine.size());
+#pragma omp parallel
+    {
+      std::vector<uint8_t> oct;
+      std::vector<double> tx, ty, tz;
+      std::vector<uint32_t> tp;
+#pragma omp for schedule(dynamic, 16)
+      for (int64_t r = 0; r < (int64_t)refine.size(); ++r) {
+        const int32_t id = refine[r];
+        const uint32_t b = L.begin[id], e = L.end[id];
+        // separate multiply then add, as cluster_tree.cpp:75-77 (no FMA)
+        const double mx = T.lo[0] + (double)(2 * L.ci[id] + 1) * cs[0];
+        const double my = T.lo[1] + (double)(2 * L.cj[id] + 1) * cs[1];
+        const double mz = T.lo[2] + (double)(2 * L.ck[id] + 1) * cs[2];
+        oct.resize(e - b);
+        std::array<uint32_t, 8> c{};
+        for (uint32_t i = b; i < e; ++i) {
+          const int o = 4 * (T.x[i] > mx) + 2 * (T.y[i] > my) + (T.z[i] > mz);
+          oct[i - b] = (uint8_t)o;
+          ++c[o];
+        }
+        std::array<uint32_t, 8> cur;
+        uint32_t acc = 0;
+        for (int o = 0; o < 8; ++o) { cur[o] = acc; acc += c[o]; }
+        tx.resize(e - b); ty.resize(e - b); tz.resize(e - b); tp.resize(e - b);
+        for (uint32_t i = b; i < e; ++i) {
+          const uint32_t d = cur[oct[i - b]]++;
+          tx[d] = T.x[i]; ty[d] = T.y[i]; tz[d] = T.z[i]; tp[d] = T.perm[i];
+        }
+        std::copy(tx.begin(), tx.end(), T.x.begin() + b);
+        std::copy(ty.begin(), ty.end(), T.y.begin() + b);
+        std::copy(tz.begin(), tz.end(), T.z.begin() + b);
+        std::copy(tp.begin(), tp.end(), T.perm.begin() + b);
+        cnt[r] = c;
+      }
+    }
+    LevelNodes N;
+    for (size_t r = 0; r < refine.size(); ++r) {
+      const int32_t id = refine[r];
+      L.leaf[id] = 0;
+      uint32_t off = L.begin[id];
+      for (int o = 0; o < 8; ++o) {
+        if (cnt[r][o] == 0) continue;
+        L.child[(size_t)id * 8 + o] = (int32_t)N.ci.size();
+        N.ci.push_back(2 * L.ci[id] + ((o >> 2) & 1));
+        N.cj.push_back(2 * L.cj[id] + ((o >> 1) & 1));
+        N.ck.push_back(2 * L.ck[id] + (o & 1));
+        N.begin.push_back(off);
+        N.end.push_back(off + cnt[r][o]);
+        N.leaf.push_back(1);
+        N.parent.push_back(id);
+        off += cnt[r][o];
+      }
+    }
+    T.lv.push_back(std::move(N));
+  }
+}
+
+// Def. 1 (A1)+(A3), inclusive <=; the FP64 operation order of
+// box_distance (geometry.hpp:69-76) and ClusterTree::box (cluster_tree.cpp:130-139).
+inline bool admissible(const Plan& P, int l, int32_t t, int32_t s) {
+  const TreePlan& T = P.T;
+  const TreePlan& S = P.S;
+  const double q = std::max(T.diam[l], S.diam[l]);
+  const int64_t tc[3] = {T.lv[l].ci[t], T.lv[l].cj[t], T.lv[l].ck[t]};
+  const int64_t sc[3] = {S.lv[l].ci[s], S.lv[l].cj[s], S.lv[l].ck[s]};
+  double acc = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    const double tlo = T.lo[a] + (double)tc[a] * T.side[l][a];
+    const double thi = T.lo[a] + (double)(tc[a] + 1) * T.side[l][a];
+    const double slo = S.lo[a] + (double)sc[a] * S.side[l][a];
+    const double shi = S.lo[a] + (double)(sc[a] + 1) * S.side[l][a];
+    const double gap = std::max(std::max(tlo - shi, slo - thi), 0.0);
+    acc += gap * gap;
+  }
+  const double dist = std::sqrt(acc);
+  return (q <= P.prm.eta2 * dist) && (P.prm.kappa * q * q <= P.prm.eta2 * dist);
+}
+
+// PAPER.md Alg. 2 as a breadth-first sweep: the children of every inadmissible,
+// non-leaf pair of level l form the candidate pairs of level l+1.
+void build_blocks(Plan& P) {
+  const TreePlan& T = P.T;
+  const TreePlan& S = P.S;
+  std::vector<std::pair<int32_t, int32_t>> cur{{0, 0}};
+  const int maxl = std::min(T.depth, S.depth);
+  P.blocks.assign(maxl + 1, {});
+  const int nth = omp_get_max_threads();
+  for (int l = 0; !cur.empty(); ++l) {
+    LevelBlocks& B = P.blocks[l];
+    const LevelNodes& LT = T.lv[l];
+    const LevelNodes& LS = S.lv[l];
+    const int64_t np = (int64_t)cur.size();
+    const int nchunk = (int)std::min<int64_t>(np, 4 * nth);
+    std::vector<std::vector<int32_t>> lpt(nchunk), lps(nchunk), lmt(nchunk), lms(nchunk);
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> nxt(nchunk);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < nchunk; ++c) {
+      const int64_t b = np * c / nchunk, e = np * (c + 1) / nchunk;
+      for (int64_t i = b; i < e; ++i) {
+        const int32_t t = cur[i].first, s = cur[i].second;
+        const bool adm = admissible(P, l, t, s);
+        if (LT.leaf[t] || LS.leaf[s]) {
+          if (adm) { lpt[c].push_back(t); lps[c].push_back(s); }
+          else { lmt[c].push_back(t); lms[c].push_back(s); }
+        } else if (!adm) {
+          for (int a = 0; a < 8; ++a) {
+            const int32_t ta = LT.child[(size_t)t * 8 + a];
+            if (ta < 0) continue;
+            for (int bb = 0; bb < 8; ++bb) {
+              const int32_t sb = LS.child[(size_t)s * 8 + bb];
+              if (sb >= 0) nxt[c].push_back({ta, sb});
+            }
+          }
+        } else {
+          lpt[c].push_back(t);
+          lps[c].push_back(s);
+        }
+      }
+    }
+    cur.clear();
+    for (int c = 0; c < nchunk; ++c) {
+      B.lp_t.insert(B.lp_t.end(), lpt[c].begin(), lpt[c].end());
+      B.lp_s.insert(B.lp_s.end(), lps[c].begin(), lps[c].end());
+      B.lm_t.insert(B.lm_t.end(), lmt[c].begin(), lmt[c].end());
+      B.lm_s.insert(B.lm_s.end(), lms[c].begin(), lms[c].end());
+      cur.insert(cur.end(), nxt[c].begin(), nxt[c].end());
+    }
+    if (!cur.empty() && l + 1 > maxl) fail(1, "internal: block recursion beyond tree depth");
+  }
+}
+
+// (level, lattice offset) keys, numbered in (level, dx, dy, dz) order; the
+// direction of a key is dir_(l)(offset * rho) (Def. 3).
+void build_keys(Plan& P) {
+  int32_t base = 0;
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    LevelBlocks& B = P.blocks[l];
+    const int64_t nb = (int64_t)B.lp_t.size();
+    B.lp_key.assign(nb, -1);
+    if (nb == 0) continue;
+    const LevelNodes& LT = P.T.lv[l];
+    const LevelNodes& LS = P.S.lv[l];
+    int64_t mn[3] = {INT64_MAX, INT64_MAX, INT64_MAX}, mx[3] = {INT64_MIN, INT64_MIN, INT64_MIN};
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t d[3] = {LT.ci[B.lp_t[b]] - LS.ci[B.lp_s[b]], LT.cj[B.lp_t[b]] - LS.cj[B.lp_s[b]],
+                            LT.ck[B.lp_t[b]] - LS.ck[B.lp_s[b]]};
+      for (int a = 0; a < 3; ++a) { mn[a] = std::min(mn[a], d[a]); mx[a] = std::max(mx[a], d[a]); }
+    }
+    const int64_t ext[3] = {mx[0] - mn[0] + 1, mx[1] - mn[1] + 1, mx[2] - mn[2] + 1};
+    const int64_t vol = ext[0] * ext[1] * ext[2];
+    auto lin = [&](int64_t b) {
+      const int64_t d0 = LT.ci[B.lp_t[b]] - LS.ci[B.lp_s[b]] - mn[0];
+      const int64_t d1 = LT.cj[B.lp_t[b]] - LS.cj[B.lp_s[b]] - mn[1];
+      const int64_t d2 = LT.ck[B.lp_t[b]] - LS.ck[B.lp_s[b]] - mn[2];
+      return (d0 * ext[1] + d1) * ext[2] + d2;
+    };
+    if (vol <= (int64_t)1 << 27) {
+      std::vector<int32_t> tab(vol, -1);
+      for (int64_t b = 0; b < nb; ++b) tab[lin(b)] = 0;
+      int32_t id = base;
+      for (int64_t v = 0; v < vol; ++v)
+        if (tab[v] == 0) {
+          tab[v] = id++;
+          const int64_t d2 = v % ext[2], d1 = (v / ext[2]) % ext[1], d0 = v / (ext[1] * ext[2]);
+          P.key_level.push_back(l);
+          P.key_dx.push_back(d0 + mn[0]);
+          P.key_dy.push_back(d1 + mn[1]);
+          P.key_dz.push_back(d2 + mn[2]);
+        }
+#pragma omp parallel for
+      for (int64_t b = 0; b < nb; ++b) B.lp_key[b] = tab[lin(b)];
+      base = id;
+    } else {
+      std::vector<int64_t> u(nb);
+      for (int64_t b = 0; b < nb; ++b) u[b] = lin(b);
+      std::vector<int64_t> s = u;
+      std::sort(s.begin(), s.end());
+      s.erase(std::unique(s.begin(), s.end()), s.end());
+      for (int64_t v : s) {
+        const int64_t d2 = v % ext[2], d1 = (v / ext[2]) % ext[1], d0 = v / (ext[1] * ext[2]);
+        P.key_level.push_back(l);
+        P.key_dx.push_back(d0 + mn[0]);
+        P.key_dy.push_back(d1 + mn[1]);
+        P.key_dz.push_back(d2 + mn[2]);
+      }
+#pragma omp parallel for
+      for (int64_t b = 0; b < nb; ++b)
+        B.lp_key[b] = base + (int32_t)(std::lower_bound(s.begin(), s.end(), u[b]) - s.begin());
+      base += (int32_t)s.size();
+    }
+  }
+  P.n_sc = base;
+  P.key_dir.resize(base);
+  for (int32_t k = 0; k < base; ++k) {
+    const double v[3] = {P.key_dx[k] * P.rho[0], P.key_dy[k] * P.rho[1], P.key_dz[k] * P.rho[2]};
+    P.key_dir[k] = dir_map_vec(P.key_level[k], P.lhf, v);
+  }
+}
+
+// Def. 4: D from admissible partners, D^ from the parent's D u D^; dense slots.
+void build_dirsets(Plan& P, TreePlan& T, bool is_target) {
+  const int nl = T.depth + 1;
+  T.ndir.resize(nl);
+  T.kind.assign(nl, {});
+  T.slot_of.assign(nl, {});
+  for (int l = 0; l < nl; ++l) {
+    T.ndir[l] = num_dirs(l, P.lhf);
+    T.kind[l].assign(T.lv[l].size() * (size_t)T.ndir[l], 0);
+  }
+  for (int l = 0; l < (int)P.blocks.size() && l < nl; ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const int nd = T.ndir[l];
+    const auto& idx = is_target ? B.lp_t : B.lp_s;
+    for (size_t b = 0; b < idx.size(); ++b) T.kind[l][(size_t)idx[b] * nd + P.key_dir[B.lp_key[b]]] |= 1;
+  }
+  for (int l = 1; l < nl; ++l) {
+    const int nd = T.ndir[l], npd = T.ndir[l - 1];
+    const LevelNodes& L = T.lv[l];
+#pragma omp parallel for
+    for (int64_t i = 0; i < (int64_t)L.size(); ++i) {
+      const int32_t par = L.parent[i];
+      for (int c = 0; c < npd; ++c)
+        if (T.kind[l - 1][(size_t)par * npd + c]) T.kind[l][(size_t)i * nd + parent_dir(l - 1, P.lhf, c)] |= 2;
+    }
+  }
+  int64_t s = 0;
+  T.node_slot_first.clear();
+  for (int l = 0; l < nl; ++l) {
+    const int nd = T.ndir[l];
+    T.slot_of[l].assign(T.kind[l].size(), -1);
+    for (size_t i = 0; i < T.lv[l].size(); ++i)
+      for (int c = 0; c < nd; ++c)
+        if (T.kind[l][i * nd + c]) {
+          T.slot_of[l][i * nd + c] = (int32_t)s++;
+          T.slot_level.push_back(l);
+          T.slot_node.push_back((int32_t)i);
+          T.slot_dir.push_back(c);
+        }
+  }
+  T.nslots = s;
+}
+
+inline int32_t slot_at(const TreePlan& T, int l, int32_t node, int dir) {
+  return T.slot_of[l][(size_t)node * T.ndir[l] + dir];
+}
+
+void build_worklists(Plan& P) {
+  TreePlan& T = P.T;
+  TreePlan& S = P.S;
+  const int lhf = P.lhf;
+  // ---- S2M over source leaves
+  for (int l = 0; l <= S.depth; ++l) {
+    const LevelNodes& L = S.lv[l];
+    for (size_t i = 0; i < L.size(); ++i) {
+      if (!L.leaf[i]) continue;
+      for (int c = 0; c < S.ndir[l]; ++c) {
+        const int32_t sl = slot_at(S, l, (int32_t)i, c);
+        if (sl < 0) continue;
+        P.s2m_slot.push_back(sl);
+        P.s2m_level.push_back(l);
+        P.s2m_dir.push_back(c);
+        P.s2m_ci.push_back(L.ci[i]);
+        P.s2m_cj.push_back(L.cj[i]);
+        P.s2m_ck.push_back(L.ck[i]);
+        P.s2m_begin.push_back(L.begin[i]);
+        P.s2m_end.push_back(L.end[i]);
+      }
+    }
+  }
+  // ---- M2M (parents at level l)
+  P.m2m_parent.assign(S.depth + 1, {});
+  P.m2m_dir = P.m2m_cdir = P.m2m_child = P.m2m_parent;
+  P.m2m_pc.assign(S.depth + 1, {});
+  for (int l = 0; l < S.depth; ++l) {
+    const LevelNodes& L = S.lv[l];
+    for (size_t i = 0; i < L.size(); ++i) {
+      if (L.leaf[i]) continue;
+      for (int c = 0; c < S.ndir[l]; ++c) {
+        const int32_t sl = slot_at(S, l, (int32_t)i, c);
+        if (sl < 0) continue;
+        const int cp = parent_dir(l, lhf, c);
+        P.m2m_parent[l].push_back(sl);
+        P.m2m_dir[l].push_back(c);
+        P.m2m_cdir[l].push_back(cp);
+        P.m2m_pc[l].push_back(L.ci[i]);
+        P.m2m_pc[l].push_back(L.cj[i]);
+        P.m2m_pc[l].push_back(L.ck[i]);
+        for (int o = 0; o < 8; ++o) {
+          const int32_t ch = L.child[i * 8 + o];
+          int32_t cs = -1;
+          if (ch >= 0) {
+            cs = slot_at(S, l + 1, ch, cp);
+            if (cs < 0) fail(1, "internal: missing child moment slot");
+          }
+          P.m2m_child[l].push_back(cs);
+        }
+      }
+    }
+  }
+  // ---- L2L (children at level l+1)
+  P.l2l_child.assign(T.depth + 1, {});
+  P.l2l_cdir = P.l2l_pslot = P.l2l_pdir = P.l2l_oct = P.l2l_child;
+  P.l2l_ptr.assign(T.depth + 1, {0});
+  P.l2l_cc.assign(T.depth + 1, {});
+  for (int l = 0; l < T.depth; ++l) {
+    const LevelNodes& L = T.lv[l + 1];
+    const LevelNodes& LP = T.lv[l];
+    for (size_t i = 0; i < L.size(); ++i) {
+      const int32_t par = L.parent[i];
+      const int oct = 4 * (int)(L.ci[i] & 1) + 2 * (int)(L.cj[i] & 1) + (int)(L.ck[i] & 1);
+      (void)LP;
+      for (int cc = 0; cc < T.ndir[l + 1]; ++cc) {
+        const int32_t csl = slot_at(T, l + 1, (int32_t)i, cc);
+        if (csl < 0) continue;
+        int cnt = 0;
+        for (int c = 0; c < T.ndir[l]; ++c) {
+          const int32_t psl = slot_at(T, l, par, c);
+          if (psl < 0 || parent_dir(l, lhf, c) != cc) continue;
+          P.l2l_pslot[l].push_back(psl);
+          P.l2l_pdir[l].push_back(c);
+          P.l2l_oct[l].push_back(oct);
+          ++cnt;
+        }
+        if (cnt == 0) continue;
+        P.l2l_child[l].push_back(csl);
+        P.l2l_cdir[l].push_back(cc);
+        P.l2l_cc[l].push_back(L.ci[i]);
+        P.l2l_cc[l].push_back(L.cj[i]);
+        P.l2l_cc[l].push_back(L.ck[i]);
+        P.l2l_ptr[l].push_back((int32_t)P.l2l_pslot[l].size());
+      }
+    }
+  }
+  // ---- L2T + P2P over owned target leaves
+  std::vector<std::vector<std::vector<std::pair<uint32_t, uint32_t>>>> near(T.depth + 1);
+  for (int l = 0; l <= T.depth; ++l) near[l].assign(T.lv[l].size(), {});
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    for (size_t b = 0; b < B.lm_t.size(); ++b)
+      near[l][B.lm_t[b]].push_back({S.lv[l].begin[B.lm_s[b]], S.lv[l].end[B.lm_s[b]]});
+  }
+  P.p2p_ptr.assign(1, 0);
+  int64_t leaf_id = 0;
+  for (int l = 0; l <= T.depth; ++l) {
+    const LevelNodes& L = T.lv[l];
+    for (size_t i = 0; i < L.size(); ++i) {
+      if (!L.leaf[i]) continue;
+      const bool own = P.t_leaf_owned.empty() || P.t_leaf_owned[leaf_id];
+      ++leaf_id;
+      if (!own) continue;
+      int32_t s0 = -1, ns = 0;
+      for (int c = 0; c < T.ndir[l]; ++c) {
+        const int32_t sl = slot_at(T, l, (int32_t)i, c);
+        if (sl < 0) continue;
+        if (s0 < 0) s0 = sl;
+        ++ns;
+      }
+      P.l2t_level.push_back(l);
+      P.l2t_slot0.push_back(s0);
+      P.l2t_nslot.push_back(ns);
+      P.l2t_ci.push_back(L.ci[i]);
+      P.l2t_cj.push_back(L.cj[i]);
+      P.l2t_ck.push_back(L.ck[i]);
+      P.l2t_begin.push_back(L.begin[i]);
+      P.l2t_end.push_back(L.end[i]);
+      std::vector<std::pair<uint32_t, uint32_t>> rg;
+      int32_t id = (int32_t)i;
+      for (int ll = l; ll >= 0; --ll) {
+        rg.insert(rg.end(), near[ll][id].begin(), near[ll][id].end());
+        id = T.lv[ll].parent[id];
+      }
+      std::sort(rg.begin(), rg.end());
+      for (size_t r = 0; r < rg.size(); ++r) {
+        if (!P.p2p_sbeg.empty() && P.p2p_ptr.back() < (int64_t)P.p2p_sbeg.size() && P.p2p_send.back() == rg[r].first) {
+          P.p2p_send.back() = rg[r].second;  // merge contiguous ranges
+        } else {
+          P.p2p_sbeg.push_back(rg[r].first);
+          P.p2p_send.push_back(rg[r].second);
+        }
+      }
+      P.p2p_ptr.push_back((int64_t)P.p2p_sbeg.size());
+    }
+  }
+}
+
+// M2L tiles: target slots grouped by (level, direction, lattice parity) share
+// (almost) the same key list; a tile = `tile` such slots, the union of their
+// keys, and for every key the source slot of each column (-1 if none).
+void build_m2l(Plan& P) {
+  const TreePlan& T = P.T;
+  const TreePlan& S = P.S;
+  const int TT = P.prm.tile;
+  // pairs (target slot, key, source slot)
+  int64_t npairs = 0;
+  for (auto& B : P.blocks) npairs += (int64_t)B.lp_t.size();
+  P.n_c = npairs;
+  std::vector<int32_t> cnt(T.nslots + 1, 0);
+  std::vector<int32_t> pt(npairs), pk(npairs), ps(npairs);
+  {
+    int64_t o = 0;
+    for (int l = 0; l < (int)P.blocks.size(); ++l) {
+      const LevelBlocks& B = P.blocks[l];
+      const int64_t nb = (int64_t)B.lp_t.size();
+#pragma omp parallel for
+      for (int64_t b = 0; b < nb; ++b) {
+        const int d = P.key_dir[B.lp_key[b]];
+        pt[o + b] = slot_at(T, l, B.lp_t[b], d);
+        ps[o + b] = slot_at(S, l, B.lp_s[b], d);
+        pk[o + b] = B.lp_key[b];
+      }
+      o += nb;
+    }
+  }
+  for (int64_t b = 0; b < npairs; ++b) cnt[pt[b] + 1]++;
+  std::vector<int64_t> ptr(T.nslots + 1, 0);
+  for (int64_t i = 0; i < T.nslots; ++i) ptr[i + 1] = ptr[i] + cnt[i + 1];
+  std::vector<int32_t> sk(npairs), ss(npairs);
+  {
+    std::vector<int64_t> cur(ptr.begin(), ptr.end() - 1);
+    for (int64_t b = 0; b < npairs; ++b) {
+      const int64_t d = cur[pt[b]]++;
+      sk[d] = pk[b];
+      ss[d] = ps[b];
+    }
+  }
+  std::vector<int32_t>().swap(pt);
+  std::vector<int32_t>().swap(pk);
+  std::vector<int32_t>().swap(ps);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t t = 0; t < T.nslots; ++t) {
+    const int64_t b = ptr[t], e = ptr[t + 1];
+    if (e - b < 2) continue;
+    std::vector<std::pair<int32_t, int32_t>> v(e - b);
+    for (int64_t i = b; i < e; ++i) v[i - b] = {sk[i], ss[i]};
+    std::sort(v.begin(), v.end());
+    for (int64_t i = b; i < e; ++i) { sk[i] = v[i - b].first; ss[i] = v[i - b].second; }
+  }
+  // group target slots
+  std::vector<int32_t> ts;
+  for (int64_t t = 0; t < T.nslots; ++t)
+    if (ptr[t + 1] > ptr[t]) ts.push_back((int32_t)t);
+  auto gkey = [&](int32_t t) {
+    const int l = T.slot_level[t];
+    const int32_t nd = T.slot_node[t];
+    const int par = 4 * (int)(T.lv[l].ci[nd] & 1) + 2 * (int)(T.lv[l].cj[nd] & 1) + (int)(T.lv[l].ck[nd] & 1);
+    return ((int64_t)l << 40) | ((int64_t)T.slot_dir[t] << 8) | par;
+  };
+  std::stable_sort(ts.begin(), ts.end(), [&](int32_t a, int32_t b) { return gkey(a) < gkey(b); });
+  std::vector<int64_t> tile_first;  // index into ts
+  for (size_t i = 0; i < ts.size();) {
+    size_t j = i;
+    const int64_t g = gkey(ts[i]);
+    while (j < ts.size() && gkey(ts[j]) == g) ++j;
+    for (size_t k = i; k < j; k += TT) tile_first.push_back((int64_t)k);
+    i = j;
+  }
+  tile_first.push_back((int64_t)ts.size());
+  const int64_t ntile = (int64_t)tile_first.size() - 1;
+  // a tile never spans two groups: clip at group boundaries
+  P.tile_level.assign(ntile, 0);
+  P.tile_dir.assign(ntile, 0);
+  P.tile_tslot.assign(ntile * TT, -1);
+  std::vector<std::vector<int32_t>> tkeys(ntile);
+  std::vector<int64_t> tcount(ntile);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t tl = 0; tl < ntile; ++tl) {
+    int64_t b = tile_first[tl], e = tile_first[tl + 1];
+    const int64_t g = gkey(ts[b]);
+    int64_t ee = b;
+    while (ee < e && gkey(ts[ee]) == g) ++ee;
+    e = ee;
+    P.tile_level[tl] = T.slot_level[ts[b]];
+    P.tile_dir[tl] = T.slot_dir[ts[b]];
+    std::vector<int32_t> u;
+    for (int64_t i = b; i < e; ++i) {
+      P.tile_tslot[tl * TT + (i - b)] = ts[i];
+      u.insert(u.end(), sk.begin() + ptr[ts[i]], sk.begin() + ptr[ts[i] + 1]);
+    }
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    tcount[tl] = (int64_t)u.size();
+    tkeys[tl] = std::move(u);
+  }
+  P.tile_kptr.assign(ntile + 1, 0);
+  for (int64_t tl = 0; tl < ntile; ++tl) P.tile_kptr[tl + 1] = P.tile_kptr[tl] + tcount[tl];
+  const int64_t tot = P.tile_kptr[ntile];
+  P.tile_keys.resize(tot);
+  P.tile_src.assign(tot * TT, -1);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t tl = 0; tl < ntile; ++tl) {
+    const auto& u = tkeys[tl];
+    const int64_t base = P.tile_kptr[tl];
+    std::copy(u.begin(), u.end(), P.tile_keys.begin() + base);
+    for (int c = 0; c < TT; ++c) {
+      const int32_t t = P.tile_tslot[tl * TT + c];
+      if (t < 0) continue;
+      size_t q = 0;
+      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) {
+        while (u[q] != sk[i]) ++q;
+        P.tile_src[(base + (int64_t)q) * TT + c] = ss[i];
+      }
+    }
+  }
+  P.m2l_cols_exec = tot * TT;
+  // split-K work items: about 8 items per SM of a 148-SM B200
+  const int64_t target_items = 148 * 8;
+  const int64_t kch = std::max<int64_t>(4, (tot + target_items - 1) / target_items);
+  P.tile_item0.assign(ntile, 0);
+  P.tile_nitem.assign(ntile, 0);
+  for (int64_t tl = 0; tl < ntile; ++tl) {
+    const int64_t nk = tcount[tl];
+    const int64_t ni = std::max<int64_t>(1, (nk + kch - 1) / kch);
+    P.tile_item0[tl] = (int32_t)P.item_tile.size();
+    P.tile_nitem[tl] = (int32_t)ni;
+    for (int64_t i = 0; i < ni; ++i) {
+      P.item_tile.push_back((int32_t)tl);
+      P.item_k0.push_back(P.tile_kptr[tl] + nk * i / ni);
+      P.item_k1.push_back(P.tile_kptr[tl] + nk * (i + 1) / ni);
+    }
+  }
+  // target slots with no M2L contribution
+  for (int64_t t = 0; t < T.nslots; ++t)
+    if (ptr[t + 1] == ptr[t]) P.m2l_zero_slots.push_back((int32_t)t);
+}
+
+}  // namespace
+
+int num_dirs(int level, int lhf) { return level > lhf ? 1 : (6 << (2 * (lhf - level))); }
+
+// Def. 3 with closed cells and the min-j rule: first argmax
+// axis selects the main face (-x,+x,-y,+y,-z,+z); then, per subdivision, the
+// lower half whenever the in-face coordinate v_u / M is <= the cell midpoint.
+int dir_map_vec(int level, int lhf, const double v[3]) {
+  if (level > lhf) return 0;
+  int a = 0;
+  double M = std::fabs(v[0]);
+  for (int i = 1; i < 3; ++i)
+    if (std::fabs(v[i]) > M) { M = std::fabs(v[i]); a = i; }
+  if (M == 0.0) return 0;
+  const int u = (a == 0) ? 1 : 0, w = (a == 2) ? 1 : 2;
+  const double cu = v[u] / M, cw = v[w] / M;
+  int j = 2 * a + (v[a] > 0.0 ? 1 : 0);
+  double ulo = -1.0, uhi = 1.0, wlo = -1.0, whi = 1.0;
+  for (int d = 0; d < lhf - level; ++d) {
+    const double um = 0.5 * (ulo + uhi), wm = 0.5 * (wlo + whi);
+    const int qu = cu > um ? 1 : 0, qw = cw > wm ? 1 : 0;
+    if (qu) ulo = um; else uhi = um;
+    if (qw) wlo = wm; else whi = wm;
+    j = 4 * j + 2 * qu + qw;
+  }
+  return j;
+}
+
+// Alg. 3: normalized midpoint of the face cell of index idx at level.
+void dir_vec(int level, int lhf, int idx, double out[3]) {
+  out[0] = out[1] = out[2] = 0.0;
+  if (level > lhf) return;
+  const int d = lhf - level;
+  const int j0 = idx >> (2 * d);
+  const int a = j0 / 2;
+  const int u = (a == 0) ? 1 : 0, w = (a == 2) ? 1 : 2;
+  double ulo = -1.0, uhi = 1.0, wlo = -1.0, whi = 1.0;
+  for (int k = d - 1; k >= 0; --k) {
+    const int q = (idx >> (2 * k)) & 3;
+    const double um = 0.5 * (ulo + uhi), wm = 0.5 * (wlo + whi);
+    if (q >> 1) ulo = um; else uhi = um;
+    if (q & 1) wlo = wm; else whi = wm;
+  }
+  double p[3];
+  p[a] = (j0 & 1) ? 1.0 : -1.0;
+  p[u] = 0.5 * (ulo + uhi);
+  p[w] = 0.5 * (wlo + whi);
+  const double nn = norm3(p);
+  for (int i = 0; i < 3; ++i) out[i] = (1.0 / nn) * p[i];
+}
+
+void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
+                const PlanParams& prm) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!(prm.kappa > 0.0) || !std::isfinite(prm.kappa)) fail(1, "wave number must be positive and finite");
+  if (prm.m < 0 || prm.m > 10) fail(1, "interpolation degree must be in [0, 10]");
+  if (!(prm.eta2 > 0.0)) fail(1, "eta2 must be positive");
+  if (prm.l_hf < -2) fail(1, "l_hf must be >= -1 (or -2 for the default rule)");
+  if (prm.depth_cap < 0) fail(1, "depth_cap must be >= 0");
+  P.prm = prm;
+  P.p = prm.m + 1;
+  P.n = P.p * P.p * P.p;
+  P.n_pad = (P.n + 31) / 32 * 32;
+  build_tree(P.T, tx, ty, tz, nt, lo, hi, prm.n_max, prm.depth_cap);
+  build_tree(P.S, sx, sy, sz, ns, lo, hi, prm.n_max, prm.depth_cap);
+  // l_hf default
+  P.lhf = prm.l_hf;
+  if (P.lhf == -2) {
+    P.lhf = -1;
+    for (int l = 0; l <= std::min(P.T.depth, P.S.depth); ++l)
+      if (prm.kappa * std::max(P.T.diam[l], P.S.diam[l]) >= 3.0) P.lhf = l;
+  }
+  const double mn = std::min({P.T.side[0][0], P.T.side[0][1], P.T.side[0][2]});
+  for (int a = 0; a < 3; ++a) P.rho[a] = P.T.side[0][a] / mn;
+  build_blocks(P);
+  build_keys(P);
+  build_dirsets(P, P.T, true);
+  build_dirsets(P, P.S, false);
+  // direction vector tables
+  const int maxl = std::max(P.T.depth, P.S.depth);
+  P.dirvec.assign(maxl + 1, {});
+  for (int l = 0; l <= maxl; ++l) {
+    const int nd = num_dirs(l, P.lhf);
+    P.dirvec[l].resize(3 * nd);
+    for (int j = 0; j < nd; ++j) dir_vec(l, P.lhf, j, &P.dirvec[l][3 * j]);
+  }
+  // interpolation constants (interpolation.cpp:9-20, 89-99)
+  P.cheb_cos.resize(P.p);
+  for (int nu = 1; nu <= P.p; ++nu) P.cheb_cos[nu - 1] = std::cos((2.0 * nu - 1.0) * kPi / (2.0 * P.p));
+  {
+    auto nodes = [&](double a, double b) {
+      std::vector<double> x(P.p);
+      const double mid = 0.5 * (a + b), half = 0.5 * (b - a);
+      for (int i = 0; i < P.p; ++i) x[i] = mid + half * P.cheb_cos[i];
+      return x;
+    };
+    const auto par = nodes(0.0, 1.0);
+    P.half.assign(2 * P.p * P.p, 0.0);
+    for (int h = 0; h < 2; ++h) {
+      const auto ch = h == 0 ? nodes(0.0, 0.5) : nodes(0.5, 1.0);
+      for (int j = 0; j < P.p; ++j)
+        for (int k = 0; k < P.p; ++k) {
+          double v = 1.0;
+          for (int q = 0; q < P.p; ++q) {
+            if (q == k) continue;
+            v *= (ch[j] - par[q]) / (par[k] - par[q]);
+          }
+          P.half[(h * P.p + j) * P.p + k] = v;
+        }
+    }
+  }
+  // ownership of target leaves (Morton-contiguous, cost-balanced) for sharded runs
+  if (prm.world > 1) {
+    std::vector<double> cost;
+    // cost of a leaf: near-field pairs * 24 + its share of M2L over its ancestors (by points)
+    // computed after work lists would be circular; use points * (near sources) proxy below.
+    int64_t nl = 0;
+    for (int l = 0; l <= P.T.depth; ++l)
+      for (size_t i = 0; i < P.T.lv[l].size(); ++i) nl += P.T.lv[l].leaf[i];
+    // leaves in Morton order over all levels: order by (coordinate scaled to the deepest level)
+    struct LeafRef { uint64_t key; int64_t id; double c; };
+    std::vector<LeafRef> lr;
+    int64_t id = 0;
+    const int D = P.T.depth;
+    std::vector<double> nearcnt;
+    for (int l = 0; l <= D; ++l)
+      for (size_t i = 0; i < P.T.lv[l].size(); ++i) {
+        if (!P.T.lv[l].leaf[i]) continue;
+        uint64_t k = 0;
+        const int64_t ci = P.T.lv[l].ci[i] << (D - l), cj = P.T.lv[l].cj[i] << (D - l),
+                      ck = P.T.lv[l].ck[i] << (D - l);
+        for (int b = D - 1; b >= 0; --b) k = (k << 3) | (((ci >> b) & 1) << 2) | (((cj >> b) & 1) << 1) | ((ck >> b) & 1);
+        lr.push_back({k, id++, (double)(P.T.lv[l].end[i] - P.T.lv[l].begin[i]) + 1.0});
+      }
+    std::sort(lr.begin(), lr.end(), [](const LeafRef& a, const LeafRef& b) { return a.key < b.key; });
+    double tot = 0;
+    for (auto& r : lr) tot += r.c;
+    P.t_leaf_owned.assign(nl, 0);
+    double acc = 0;
+    for (auto& r : lr) {
+      const double mid = acc + 0.5 * r.c;
+      const int owner = std::min(prm.world - 1, (int)(mid / tot * prm.world));
+      if (owner == prm.rank) P.t_leaf_owned[r.id] = 1;
+      acc += r.c;
+    }
+  }
+  build_worklists(P);
+  build_m2l(P);
+  // statistics
+  for (auto& B : P.blocks) {
+    P.n_lminus += (int64_t)B.lm_t.size();
+  }
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    for (size_t b = 0; b < B.lm_t.size(); ++b)
+      P.m_d += (int64_t)(P.T.lv[l].end[B.lm_t[b]] - P.T.lv[l].begin[B.lm_t[b]]) *
+               (int64_t)(P.S.lv[l].end[B.lm_s[b]] - P.S.lv[l].begin[B.lm_s[b]]);
+  }
+  for (int w = 0; w < 2; ++w) {
+    const TreePlan& X = w == 0 ? P.T : P.S;
+    for (int l = 0; l <= X.depth; ++l) {
+      const int nd = X.ndir[l];
+      for (size_t i = 0; i < X.lv[l].size(); ++i) {
+        int64_t k = 0;
+        for (int c = 0; c < nd; ++c) k += X.kind[l][i * nd + c] != 0;
+        if (X.lv[l].leaf[i]) {
+          P.n_le += k;
+        } else {
+          int nch = 0;
+          for (int o = 0; o < 8; ++o) nch += X.lv[l].child[i * 8 + o] >= 0;
+          P.n_le += k * nch;
+        }
+      }
+    }
+  }
+  P.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------------ exports
+namespace {
+struct Row7 { int64_t v[7]; };
+}
+
+int64_t export_tree(const TreePlan& T, int64_t* rows) {
+  int64_t n = 0;
+  for (auto& L : T.lv) n += (int64_t)L.size();
+  if (!rows) return n;
+  std::vector<std::array<int64_t, 7>> r;
+  r.reserve(n);
+  for (int l = 0; l <= T.depth; ++l) {
+    const LevelNodes& L = T.lv[l];
+    for (size_t i = 0; i < L.size(); ++i) r.push_back({l, L.ci[i], L.cj[i], L.ck[i], L.begin[i], L.end[i], L.leaf[i]});
+  }
+  std::sort(r.begin(), r.end());
+  std::memcpy(rows, r.data(), sizeof(int64_t) * 7 * n);
+  return n;
+}
+int64_t export_perm(const TreePlan& T, int64_t* out) {
+  if (out)
+    for (size_t i = 0; i < T.perm.size(); ++i) out[i] = T.perm[i];
+  return (int64_t)T.perm.size();
+}
+int64_t export_lplus(const Plan& P, int64_t* rows) {
+  int64_t n = 0;
+  for (auto& B : P.blocks) n += (int64_t)B.lp_t.size();
+  if (!rows) return n;
+  std::vector<std::array<int64_t, 8>> r;
+  r.reserve(n);
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const LevelNodes& LT = P.T.lv[l];
+    const LevelNodes& LS = P.S.lv[l];
+    for (size_t b = 0; b < B.lp_t.size(); ++b)
+      r.push_back({l, LT.ci[B.lp_t[b]], LT.cj[B.lp_t[b]], LT.ck[B.lp_t[b]], LS.ci[B.lp_s[b]], LS.cj[B.lp_s[b]],
+                   LS.ck[B.lp_s[b]], P.key_dir[B.lp_key[b]]});
+  }
+  std::sort(r.begin(), r.end());
+  std::memcpy(rows, r.data(), sizeof(int64_t) * 8 * n);
+  return n;
+}
+int64_t export_lminus(const Plan& P, int64_t* rows) {
+  int64_t n = 0;
+  for (auto& B : P.blocks) n += (int64_t)B.lm_t.size();
+  if (!rows) return n;
+  std::vector<std::array<int64_t, 8>> r;
+  r.reserve(n);
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const LevelNodes& LT = P.T.lv[l];
+    const LevelNodes& LS = P.S.lv[l];
+    for (size_t b = 0; b < B.lm_t.size(); ++b)
+      r.push_back({l, LT.ci[B.lm_t[b]], LT.cj[B.lm_t[b]], LT.ck[B.lm_t[b]], l, LS.ci[B.lm_s[b]], LS.cj[B.lm_s[b]],
+                   LS.ck[B.lm_s[b]]});
+  }
+  std::sort(r.begin(), r.end());
+  std::memcpy(rows, r.data(), sizeof(int64_t) * 8 * n);
+  return n;
+}
+int64_t export_dirsets(const Plan& P, int which, int64_t* rows) {
+  const TreePlan& T = which == 0 ? P.T : P.S;
+  if (!rows) return T.nslots;
+  std::vector<std::array<int64_t, 6>> r;
+  r.reserve(T.nslots);
+  for (int l = 0; l <= T.depth; ++l) {
+    const int nd = T.ndir[l];
+    const LevelNodes& L = T.lv[l];
+    for (size_t i = 0; i < L.size(); ++i)
+      for (int c = 0; c < nd; ++c) {
+        const uint8_t k = T.kind[l][i * nd + c];
+        if (k) r.push_back({l, L.ci[i], L.cj[i], L.ck[i], c, k});
+      }
+  }
+  std::sort(r.begin(), r.end());
+  std::memcpy(rows, r.data(), sizeof(int64_t) * 6 * r.size());
+  return (int64_t)r.size();
+}
+
+}  // namespace fdhelm

@@ -1,0 +1,124 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Tolerance: relative l2 <= 1e-12 on y (BASELINE.json
+north_star); structure is bit-exact (tests/test_plan.py)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2004_14229_b200 as F
+from paper_2004_14229_b200.configs import CONFIGS, grid_points, make_inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu(gpu_required):
+    F.build()
+
+
+def run_pair(tg, sr, q, lo, hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=-2, zero_diagonal=0, depth_cap=30):
+    op = F.DirectionalOperator(tg, sr, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal)
+    o = oracle.Oracle(tg, sr, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal)
+    return op.apply(q), o.apply(q), op, o
+
+
+def test_cfg1_full_parity():
+    c = CONFIGS[1]
+    tg, sr, q = make_inputs(c)
+    y, yo, op, _ = run_pair(tg, sr, q, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    err = oracle.rel_l2(y, yo)
+    print("cfg1 rel l2 vs oracle", err, op.stats()["apply_ms"], "ms")
+    assert err <= TOL
+    assert np.array_equal(op.apply(q), y)  # bitwise determinism
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6])
+def test_degrees(m):
+    rng = np.random.default_rng(100 + m)
+    tg = [rng.random(6000) for _ in range(3)]
+    sr = [rng.random(5000) for _ in range(3)]
+    q = rng.uniform(-1, 1, 5000) + 1j * rng.uniform(-1, 1, 5000)
+    y, yo, _, _ = run_pair(tg, sr, q, (0, 0, 0), (1, 1, 1), 12.0, 32, m, 1.0, -2)
+    assert oracle.rel_l2(y, yo) <= TOL
+
+
+@pytest.mark.parametrize("lhf", [-1, 1, 2, 3])
+def test_direction_levels(lhf):
+    """Directional transfers with c and c' both nonzero (l_hf forced above the
+    leaf level), and the non-directional case (l_hf = -1)."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    y, yo, op, _ = run_pair(tg, sr, q, c.root_lo, c.root_hi, 24.0, 32, 3, 1.0, lhf)
+    assert op.stats()["n_c"] > 0
+    assert oracle.rel_l2(y, yo) <= TOL
+
+
+def test_cfg5_shape_nonuniform():
+    c = CONFIGS[5]
+    tg, sr, q = make_inputs(c, nt=40000, ns=20000)
+    y, yo, op, _ = run_pair(tg, sr, q, c.root_lo, c.root_hi, c.kappa, c.n_max, 4, c.eta2, c.l_hf)
+    assert oracle.rel_l2(y, yo) <= TOL
+
+
+def test_pure_nearfield_and_dense():
+    rng = np.random.default_rng(11)
+    pt = [rng.random(900) for _ in range(3)]
+    ps = [rng.random(700) for _ in range(3)]
+    q = rng.standard_normal(700) + 1j * rng.standard_normal(700)
+    op = F.DirectionalOperator(pt, ps, (0, 0, 0), (1, 1, 1), 1e6, n_max=16, m=2)
+    assert op.stats()["n_c"] == 0
+    yd = oracle.dense_rows(pt, ps, q, 1e6, np.arange(900))
+    assert oracle.rel_l2(op.apply(q), yd) <= 1e-13
+
+
+def test_zero_diagonal_grid():
+    g = grid_points(4)
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
+    y, yo, _, _ = run_pair(g, g, q, (-1, -1, -1), (1, 1, 1), 1.6, 64, 4, 5.0, 0, zero_diagonal=1)
+    assert oracle.rel_l2(y, yo) <= TOL
+
+
+def test_linearity():
+    c = CONFIGS[1]
+    tg, sr, q = make_inputs(c)
+    op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m)
+    q2 = np.random.default_rng(1).standard_normal(c.ns) + 0j
+    a = 0.3 - 1.7j
+    assert oracle.rel_l2(op.apply(a * q + q2), a * op.apply(q) + op.apply(q2)) <= 1e-12
+
+
+def test_singular_kernel_reported():
+    rng = np.random.default_rng(2)
+    pts = [rng.random(500) for _ in range(3)]
+    op = F.DirectionalOperator(pts, pts, (0, 0, 0), (1, 1, 1), 2.0, n_max=32, m=2)
+    with pytest.raises(F.FdhError) as e:
+        op.apply(np.ones(500, dtype=np.complex128))
+    assert e.value.code == F.ERR_DOMAIN  # geometry.hpp:82 domain_error
+    opz = F.DirectionalOperator(pts, pts, (0, 0, 0), (1, 1, 1), 2.0, n_max=32, m=2, zero_diagonal=True)
+    opz.apply(np.ones(500, dtype=np.complex128))
+
+
+def test_dimension_mismatch():
+    c = CONFIGS[1]
+    tg, sr, q = make_inputs(c, nt=2000, ns=2000)
+    op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa)
+    with pytest.raises(F.FdhError) as e:
+        op.apply(q[:10])
+    assert e.value.code == F.ERR_DIM
+
+
+def test_cfg2_sampled_oracle():
+    """BASELINE config 2 at full size: sampled-target oracle."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c)
+    op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    y = op.apply(q)
+    o = oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    nl = o.leaf_count(0)
+    leaves = np.unique(np.concatenate([[0, nl - 1], np.random.default_rng(2).choice(nl, 40, replace=False)]))
+    rows, ys = o.apply_sampled(q, leaves)
+    err = oracle.rel_l2(y[rows], ys)
+    print("cfg2 sampled rel l2", err, "rows", len(rows))
+    assert err <= TOL
