@@ -62,6 +62,7 @@ struct fdh_op {
   uint32_t *p2p_sbeg = nullptr, *p2p_send = nullptr;
   // M2L
   int n_item = 0, n_tile = 0;
+  uint8_t* tile_mask = nullptr;
   int32_t *item_tile = nullptr, *tile_keys = nullptr, *tile_src = nullptr, *tile_item0 = nullptr,
           *tile_nitem = nullptr, *tile_tslot = nullptr;
   int64_t *item_k0 = nullptr, *item_k1 = nullptr;
@@ -226,6 +227,7 @@ void setup_device(fdh_op* o) {
   o->item_k1 = o->up(P.item_k1);
   o->tile_keys = o->up(P.tile_keys);
   o->tile_src = o->up(P.tile_src);
+  o->tile_mask = o->up(P.tile_mask);
   o->tile_item0 = o->up(P.tile_item0);
   o->tile_nitem = o->up(P.tile_nitem);
   o->tile_tslot = o->up(P.tile_tslot);
@@ -292,7 +294,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   if (o->n_item > 0) {
     rec(o, FDH_NPHASES + 1, st);
     if (launch_m2l_gemm(st, np, P.prm.tile, o->n_item, o->item_tile, o->item_k0, o->item_k1, o->tile_keys,
-                        o->tile_src, o->W, o->mom, o->partial) != 0)
+                        o->tile_src, o->tile_mask, o->W, o->mom, o->partial) != 0)
       throw PlanError{4, "no M2L kernel for this n_pad / tile"};
     rec(o, FDH_NPHASES + 2, st);
     launch_m2l_reduce(st, np, P.prm.tile, o->n_tile, o->tile_item0, o->tile_nitem, o->tile_tslot, o->partial,
@@ -505,7 +507,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   for (auto& L : P.S.lv) nn += (int64_t)L.size();
   s->nodes_s = nn;
   s->gpu_launches = o->launches;
-  s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;
+  s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;  // DMMA issued
   return FDH_OK;
 }
 

@@ -122,10 +122,12 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
                                                    const int64_t* __restrict__ item_k1,
                                                    const int32_t* __restrict__ tile_keys,
                                                    const int32_t* __restrict__ tile_src,
+                                                   const uint8_t* __restrict__ tile_mask,
                                                    const double* __restrict__ W, const double* __restrict__ mom,
                                                    double* __restrict__ partial) {
   using S = M2LShape<NPAD, TT>;
   constexpr int NT = S::NT;
+  static_assert(NT <= 8, "mask has 8 bits");
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x;
@@ -145,7 +147,8 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
   const int bk = lane & 3;
   const int re_off = bpar ? S::IMOFF : 0;   // first K half: parity 0 -> Re, 1 -> Im
   const int im_off = bpar ? 0 : S::IMOFF;   // second K half: parity 0 -> -Im, 1 -> Re
-  const double sgn = bpar ? 1.0 : -1.0;
+  // sign flip of -Im by an integer xor of the sign bit (keeps the FP64 pipe for DMMA)
+  const unsigned long long sgn = bpar ? 0ull : 0x8000000000000000ull;
 
   m2l_stage<NPAD, TT>(smem, tile_src + k0 * TT, mom);
   cp_async_commit();
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
     const double* __restrict__ Wk =
         W + (int64_t)tile_keys[kk] * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
     const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
+    const unsigned msk = tile_mask[kk];  // n-tiles with at least one target that has this key
     // K half 1: columns of Re A against (Re v, Im v)
 #pragma unroll 4
     for (int ks = 0; ks < NPAD / 4; ++ks) {
@@ -167,9 +171,11 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) b[nt] = Bs[nt * 4 * S::MS + re_off + 4 * ks];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int nt = 0; nt < NT; ++nt)
+        if (msk & (1u << nt)) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+          for (int mt = 0; mt < 4; ++mt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+        }
     }
     // K half 2: columns of Im A against (-Im v, Re v)
 #pragma unroll 4
@@ -178,11 +184,14 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + NPAD + mt * 8 * S::K2 + 4 * ks);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = sgn * Bs[nt * 4 * S::MS + im_off + 4 * ks];
+      for (int nt = 0; nt < NT; ++nt)
+        b[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 4 * ks]) ^ sgn);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int nt = 0; nt < NT; ++nt)
+        if (msk & (1u << nt)) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+          for (int mt = 0; mt < 4; ++mt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+        }
     }
     __syncthreads();
     stage ^= 1;
@@ -219,16 +228,16 @@ __global__ void __launch_bounds__(256) k_m2l_reduce(const int32_t* __restrict__ 
 
 template <int NPAD, int TT>
 void run_gemm(cudaStream_t st, int n_item, const int32_t* item_tile, const int64_t* item_k0, const int64_t* item_k1,
-              const int32_t* tile_keys, const int32_t* tile_src, const double* W, const double* mom,
-              double* partial) {
+              const int32_t* tile_keys, const int32_t* tile_src, const uint8_t* tile_mask, const double* W,
+              const double* mom, double* partial) {
   using S = M2LShape<NPAD, TT>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2l_gemm<NPAD, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
     attr = true;
   }
-  k_m2l_gemm<NPAD, TT><<<n_item, S::THREADS, S::SMEM, st>>>(item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom,
-                                                            partial);
+  k_m2l_gemm<NPAD, TT><<<n_item, S::THREADS, S::SMEM, st>>>(item_tile, item_k0, item_k1, tile_keys, tile_src,
+                                                            tile_mask, W, mom, partial);
 }
 
 }  // namespace
@@ -243,15 +252,16 @@ void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int
 
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int32_t* item_tile,
                     const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
-                    const int32_t* tile_src, const double* W, const double* mom, double* partial) {
+                    const int32_t* tile_src, const uint8_t* tile_mask, const double* W, const double* mom,
+                    double* partial) {
   if (n_item <= 0) return 0;
   if (tile != 16) return 1;
   switch (n_pad) {
-    case 32: run_gemm<32, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
-    case 64: run_gemm<64, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
-    case 128: run_gemm<128, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
-    case 224: run_gemm<224, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
-    case 352: run_gemm<352, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, W, mom, partial); break;
+    case 32: run_gemm<32, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
+    case 64: run_gemm<64, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
+    case 128: run_gemm<128, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
+    case 224: run_gemm<224, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
+    case 352: run_gemm<352, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
     default: return 1;
   }
   return 0;

@@ -38,7 +38,8 @@ void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int
 // returns 0 on success, nonzero if n_pad / tile combination is not compiled
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int32_t* item_tile,
                     const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
-                    const int32_t* tile_src, const double* W, const double* mom, double* partial);
+                    const int32_t* tile_src, const uint8_t* tile_mask, const double* W, const double* mom,
+                    double* partial);
 void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_item0,
                        const int32_t* tile_nitem, const int32_t* tile_tslot, const double* partial,
                        double* loc);

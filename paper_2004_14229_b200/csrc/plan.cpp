@@ -582,7 +582,16 @@ void build_m2l(Plan& P) {
       }
     }
   }
-  P.m2l_cols_exec = tot * TT;
+  P.tile_mask.assign(tot, 0);
+  int64_t exec = 0;
+  for (int64_t i = 0; i < tot; ++i) {
+    uint8_t mk = 0;
+    for (int c = 0; c < TT; ++c)
+      if (P.tile_src[i * TT + c] >= 0) mk |= (uint8_t)(1u << (c / 4));
+    P.tile_mask[i] = mk;
+    exec += 4 * __builtin_popcount(mk);
+  }
+  P.m2l_cols_exec = exec;
   // split-K work items: about 8 items per SM of a 148-SM B200
   const int64_t target_items = 148 * 8;
   const int64_t kch = std::max<int64_t>(4, (tot + target_items - 1) / target_items);

@@ -108,6 +108,7 @@ struct Plan {
   std::vector<int64_t> tile_kptr;    // CSR into tile_keys / tile_src
   std::vector<int32_t> tile_keys;    // key ids
   std::vector<int32_t> tile_src;     // (tile_kptr[i] + kk) * T + col -> source slot or -1
+  std::vector<uint8_t> tile_mask;    // per (tile, key): bit g set if columns 4g..4g+3 are not all empty
   // split-K work items
   std::vector<int32_t> item_tile;
   std::vector<int64_t> item_k0, item_k1;
@@ -119,7 +120,7 @@ struct Plan {
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
-  int64_t m2l_cols_exec = 0;  // sum over tiles of |keys| * T
+  int64_t m2l_cols_exec = 0;  // executed target columns (4-column groups with any pair)
   double setup_ms = 0.0;
 };
 
