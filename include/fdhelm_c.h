@@ -79,6 +79,8 @@ typedef struct fdh_stats {
   int64_t m2l_flops_executed;   /* DMMA flops incl. padding / empty columns */
   double m2l_gemm_ms;           /* average M2L GEMM kernel time (timing on)  */
   int64_t timed_applies;        /* applies averaged into phase_ms            */
+  int64_t m2l_tiles, m2l_items;  /* M2L target tiles / (tile, key chunk) items */
+  int64_t m2l_chunk;            /* key ids per chunk                          */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

@@ -39,7 +39,8 @@ class FdhStats(C.Structure):
                 ("slots_t", C.c_int64), ("slots_s", C.c_int64), ("nodes_t", C.c_int64), ("nodes_s", C.c_int64),
                 ("phase_ms", C.c_double * 8), ("apply_ms", C.c_double), ("setup_ms", C.c_double),
                 ("gpu_launches", C.c_int64), ("m2l_flops_executed", C.c_int64), ("m2l_gemm_ms", C.c_double),
-                ("timed_applies", C.c_int64)]
+                ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
+                ("m2l_chunk", C.c_int64)]
 
 
 class FdhError(RuntimeError):

@@ -63,8 +63,8 @@ struct fdh_op {
   // M2L
   int n_item = 0, n_tile = 0;
   uint8_t* tile_mask = nullptr;
-  int32_t *item_tile = nullptr, *tile_keys = nullptr, *tile_src = nullptr, *tile_item0 = nullptr,
-          *tile_nitem = nullptr, *tile_tslot = nullptr;
+  int32_t *item_tile = nullptr, *tile_keys = nullptr, *tile_src = nullptr, *tile_iptr = nullptr,
+          *tile_items = nullptr, *tile_tslot = nullptr;
   int64_t *item_k0 = nullptr, *item_k1 = nullptr;
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
@@ -228,8 +228,8 @@ void setup_device(fdh_op* o) {
   o->tile_keys = o->up(P.tile_keys);
   o->tile_src = o->up(P.tile_src);
   o->tile_mask = o->up(P.tile_mask);
-  o->tile_item0 = o->up(P.tile_item0);
-  o->tile_nitem = o->up(P.tile_nitem);
+  o->tile_iptr = o->up(P.tile_iptr);
+  o->tile_items = o->up(P.tile_items);
   o->tile_tslot = o->up(P.tile_tslot);
   o->key_level = o->up(P.key_level);
   o->key_dir = o->up(P.key_dir);
@@ -297,7 +297,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
                         o->tile_src, o->tile_mask, o->W, o->mom, o->partial) != 0)
       throw PlanError{4, "no M2L kernel for this n_pad / tile"};
     rec(o, FDH_NPHASES + 2, st);
-    launch_m2l_reduce(st, np, P.prm.tile, o->n_tile, o->tile_item0, o->tile_nitem, o->tile_tslot, o->partial,
+    launch_m2l_reduce(st, np, P.prm.tile, o->n_tile, o->tile_iptr, o->tile_items, o->tile_tslot, o->partial,
                       o->loc);
     L += 2;
   }
@@ -507,6 +507,9 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   for (auto& L : P.S.lv) nn += (int64_t)L.size();
   s->nodes_s = nn;
   s->gpu_launches = o->launches;
+  s->m2l_tiles = (int64_t)P.tile_level.size();
+  s->m2l_items = (int64_t)P.item_tile.size();
+  s->m2l_chunk = P.m2l_chunk;
   s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;  // DMMA issued
   return FDH_OK;
 }

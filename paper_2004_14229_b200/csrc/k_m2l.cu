@@ -210,18 +210,18 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
 // Sum the partials of each tile's work items in item order and store the
 // locals of its target slots (planar re | im).
 template <int NPAD, int TT>
-__global__ void __launch_bounds__(256) k_m2l_reduce(const int32_t* __restrict__ tile_item0,
-                                                    const int32_t* __restrict__ tile_nitem,
+__global__ void __launch_bounds__(256) k_m2l_reduce(const int32_t* __restrict__ tile_iptr,
+                                                    const int32_t* __restrict__ tile_items,
                                                     const int32_t* __restrict__ tile_tslot,
                                                     const double* __restrict__ partial, double* __restrict__ loc) {
   const int tile = blockIdx.x;
-  const int i0 = tile_item0[tile], ni = tile_nitem[tile];
+  const int i0 = tile_iptr[tile], i1 = tile_iptr[tile + 1];
   for (int idx = threadIdx.x; idx < NPAD * 2 * TT; idx += blockDim.x) {
     const int row = idx / (2 * TT), col = idx % (2 * TT);
     const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
     if (ts < 0) continue;
     double s = 0.0;
-    for (int i = 0; i < ni; ++i) s += partial[(int64_t)(i0 + i) * NPAD * 2 * TT + idx];
+    for (int i = i0; i < i1; ++i) s += partial[(int64_t)tile_items[i] * NPAD * 2 * TT + idx];
     loc[(int64_t)ts * 2 * NPAD + ((col & 1) ? NPAD : 0) + row] = s;
   }
 }
@@ -267,15 +267,15 @@ int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int3
   return 0;
 }
 
-void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_item0,
-                       const int32_t* tile_nitem, const int32_t* tile_tslot, const double* partial, double* loc) {
+void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_iptr,
+                       const int32_t* tile_items, const int32_t* tile_tslot, const double* partial, double* loc) {
   if (n_tile <= 0 || tile != 16) return;
   switch (n_pad) {
-    case 32: k_m2l_reduce<32, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
-    case 64: k_m2l_reduce<64, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
-    case 128: k_m2l_reduce<128, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
-    case 224: k_m2l_reduce<224, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
-    case 352: k_m2l_reduce<352, 16><<<n_tile, 256, 0, st>>>(tile_item0, tile_nitem, tile_tslot, partial, loc); break;
+    case 32: k_m2l_reduce<32, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
+    case 64: k_m2l_reduce<64, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
+    case 128: k_m2l_reduce<128, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
+    case 224: k_m2l_reduce<224, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
+    case 352: k_m2l_reduce<352, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
     default: break;
   }
 }

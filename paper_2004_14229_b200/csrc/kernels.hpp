@@ -40,8 +40,8 @@ int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int3
                     const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
                     const int32_t* tile_src, const uint8_t* tile_mask, const double* W, const double* mom,
                     double* partial);
-void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_item0,
-                       const int32_t* tile_nitem, const int32_t* tile_tslot, const double* partial,
+void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_iptr,
+                       const int32_t* tile_items, const int32_t* tile_tslot, const double* partial,
                        double* loc);
 
 }  // namespace fdhelm
