@@ -116,6 +116,47 @@ __device__ __forceinline__ void m2l_stage(double* buf, const int32_t* __restrict
   }
 }
 
+// One key of one tile: C += W_key * B over K = 2 NPAD, for the n-tiles in MASK.
+template <int NPAD, int TT, unsigned MASK>
+__device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, TT>::NT][2], const double* __restrict__ Wk,
+                                        const double* Bs, int re_off, int im_off, unsigned long long sgn) {
+  using S = M2LShape<NPAD, TT>;
+  constexpr int NT = S::NT;
+  // K half 1: columns of Re A against (Re v, Im v)
+#pragma unroll 4
+  for (int ks = 0; ks < NPAD / 4; ++ks) {
+    double a[4], b[NT];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + mt * 8 * S::K2 + 4 * ks);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      if constexpr (true) {
+        if ((MASK >> nt) & 1u) b[nt] = Bs[nt * 4 * S::MS + re_off + 4 * ks];
+      }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        if ((MASK >> nt) & 1u) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+  }
+  // K half 2: columns of Im A against (-Im v, Re v)
+#pragma unroll 4
+  for (int ks = 0; ks < NPAD / 4; ++ks) {
+    double a[4], b[NT];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + NPAD + mt * 8 * S::K2 + 4 * ks);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      if ((MASK >> nt) & 1u)
+        b[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 4 * ks]) ^ sgn);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        if ((MASK >> nt) & 1u) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+  }
+}
+
 template <int NPAD, int TT>
 __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ item_tile,
                                                    const int64_t* __restrict__ item_k0,
@@ -161,37 +202,20 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
     const double* __restrict__ Wk =
         W + (int64_t)tile_keys[kk] * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
     const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
-    const unsigned msk = tile_mask[kk];  // n-tiles with at least one target that has this key
-    // K half 1: columns of Re A against (Re v, Im v)
-#pragma unroll 4
-    for (int ks = 0; ks < NPAD / 4; ++ks) {
-      double a[4], b[NT];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + mt * 8 * S::K2 + 4 * ks);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt] = Bs[nt * 4 * S::MS + re_off + 4 * ks];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        if (msk & (1u << nt)) {
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
-        }
-    }
-    // K half 2: columns of Im A against (-Im v, Re v)
-#pragma unroll 4
-    for (int ks = 0; ks < NPAD / 4; ++ks) {
-      double a[4], b[NT];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + NPAD + mt * 8 * S::K2 + 4 * ks);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        b[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 4 * ks]) ^ sgn);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        if (msk & (1u << nt)) {
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
-        }
+    // n-tiles with at least one target that has this key.  A predicated-off
+    // DMMA still occupies the tensor pipe, so the common masks get their own
+    // unrolled loops (warp-uniform branch) instead of predication.
+    switch (tile_mask[kk]) {
+      case 0xF: m2l_key<NPAD, TT, 0xF>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x3: m2l_key<NPAD, TT, 0x3>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0xC: m2l_key<NPAD, TT, 0xC>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x5: m2l_key<NPAD, TT, 0x5>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0xA: m2l_key<NPAD, TT, 0xA>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x1: m2l_key<NPAD, TT, 0x1>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x2: m2l_key<NPAD, TT, 0x2>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x4: m2l_key<NPAD, TT, 0x4>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      case 0x8: m2l_key<NPAD, TT, 0x8>(acc, Wk, Bs, re_off, im_off, sgn); break;
+      default: m2l_key<NPAD, TT, 0xF>(acc, Wk, Bs, re_off, im_off, sgn); break;
     }
     __syncthreads();
     stage ^= 1;

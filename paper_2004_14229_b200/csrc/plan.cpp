@@ -589,7 +589,10 @@ void build_m2l(Plan& P) {
     for (int c = 0; c < TT; ++c)
       if (P.tile_src[i * TT + c] >= 0) mk |= (uint8_t)(1u << (c / 4));
     P.tile_mask[i] = mk;
-    exec += 4 * __builtin_popcount(mk);
+    // masks with their own kernel loop (k_m2l.cu); other masks run all 4 n-tiles
+    const bool special = mk == 0xF || mk == 0x3 || mk == 0xC || mk == 0x5 || mk == 0xA || mk == 0x1 ||
+                         mk == 0x2 || mk == 0x4 || mk == 0x8;
+    exec += special ? 4 * __builtin_popcount(mk) : 16;
   }
   P.m2l_cols_exec = exec;
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
