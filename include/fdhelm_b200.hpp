@@ -1,0 +1,84 @@
+// fdhelm_b200.hpp -- header-only C++20 host API over the C-ABI (fdhelm_c.h).
+//
+// Mirrors the reference's C++ vocabulary so that a caller of
+//   fdhelm::ClusterTree(std::span<const Point3>, const AxisBox&, int n_max, int depth_cap)
+//   (/root/reference/proj/include/fdhelm/cluster_tree.hpp:47) and of the SPEC L4 engine
+//   setup(T_T, T_S, ..., kappa, m) / matvec(op, v) / stats(op)
+// can switch with a handful of lines.  Errors are re-thrown as
+// the reference's exception types: std::invalid_argument (FDH_ERR_ARG, DIM),
+// std::domain_error (FDH_ERR_DOMAIN, singular kernel), std::runtime_error (CUDA).
+#pragma once
+#include <complex>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fdhelm_c.h"
+
+namespace fdhelm_b200 {
+
+using Complex = std::complex<double>;
+
+struct Params {
+  double kappa = 1.0;      // WaveNumber (geometry.hpp:38-43), > 0
+  int n_max = 64;          // ClusterTree n_max (cluster_tree.hpp:47)
+  int m = 4;               // Chebyshev degree, (m+1)^3 nodes per box
+  double eta2 = 1.0;       // admissibility constant of (A1)/(A3)
+  int l_hf = FDH_LHF_DEFAULT;
+  int depth_cap = 30;
+  bool zero_diagonal = false;
+};
+
+inline void check(int rc) {
+  if (rc == FDH_OK) return;
+  const std::string msg = fdh_last_error();
+  switch (rc) {
+    case FDH_ERR_ARG:
+    case FDH_ERR_DIM: throw std::invalid_argument(msg);
+    case FDH_ERR_DOMAIN: throw std::domain_error(msg);
+    default: throw std::runtime_error("fdhelm_b200: " + msg);
+  }
+}
+
+class DirectionalOperator {
+ public:
+  // Points as SoA spans (x, y, z) of targets and sources; one shared root box.
+  DirectionalOperator(std::span<const double> tx, std::span<const double> ty, std::span<const double> tz,
+                      std::span<const double> sx, std::span<const double> sy, std::span<const double> sz,
+                      const double root_lo[3], const double root_hi[3], const Params& p)
+      : nt_(tx.size()), ns_(sx.size()) {
+    if (ty.size() != nt_ || tz.size() != nt_ || sy.size() != ns_ || sz.size() != ns_)
+      throw std::invalid_argument("coordinate arrays of one point set differ in length");
+    check(fdh_create(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(), (int64_t)ns_,
+                     root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap, p.zero_diagonal ? 1 : 0,
+                     1, &op_));
+  }
+  DirectionalOperator(const DirectionalOperator&) = delete;
+  DirectionalOperator& operator=(const DirectionalOperator&) = delete;
+  ~DirectionalOperator() { fdh_destroy(op_); }
+
+  // SPEC.md:493-501 matvec: y (N_T) = A x (N_S), original point order.
+  void apply(std::span<const Complex> x, std::span<Complex> y) {
+    if (x.size() != ns_ || y.size() != nt_) throw std::invalid_argument("matvec: dimension mismatch");
+    check(fdh_apply(op_, reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(y.data())));
+  }
+  std::vector<Complex> apply(std::span<const Complex> x) {
+    std::vector<Complex> y(nt_);
+    apply(x, y);
+    return y;
+  }
+  fdh_stats stats() const {
+    fdh_stats s{};
+    check(fdh_get_stats(op_, &s));
+    return s;
+  }
+  fdh_op* handle() { return op_; }
+
+ private:
+  size_t nt_, ns_;
+  fdh_op* op_ = nullptr;
+};
+
+}  // namespace fdhelm_b200

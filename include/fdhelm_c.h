@@ -81,6 +81,7 @@ typedef struct fdh_stats {
   int64_t timed_applies;        /* applies averaged into phase_ms            */
   int64_t m2l_tiles, m2l_items;  /* M2L target tiles / (tile, key chunk) items */
   int64_t m2l_chunk;            /* key ids per chunk                          */
+  double shard_cost, total_cost; /* estimated flops: this shard / all targets */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table
@@ -134,6 +135,9 @@ int64_t fdh_export_perm(const fdh_op* op, int which, int64_t* perm);
 int64_t fdh_export_lplus(const fdh_op* op, int64_t* rows /*8 cols*/);
 int64_t fdh_export_lminus(const fdh_op* op, int64_t* rows /*8 cols*/);
 int64_t fdh_export_dirsets(const fdh_op* op, int which, int64_t* rows /*6 cols*/);
+/* target leaves owned by this operator (all, or this rank's shard):
+ * level, i, j, k, begin, end                                        (6 cols) */
+int64_t fdh_export_owned_leaves(const fdh_op* op, int64_t* rows);
 
 void fdh_destroy(fdh_op* op);
 const char* fdh_last_error(void);

@@ -28,7 +28,7 @@ ERR_ARG, ERR_DOMAIN, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_MEMORY = 1, 2, 3, 4
 PHASES = ["h2d", "s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "d2h"]
 SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_plan_only", "fdh_apply", "fdh_apply_device", "fdh_stream",
            "fdh_set_timing", "fdh_get_stats", "fdh_export_tree", "fdh_export_perm", "fdh_export_lplus",
-           "fdh_export_lminus", "fdh_export_dirsets", "fdh_destroy", "fdh_last_error", "fdh_version",
+           "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_destroy", "fdh_last_error", "fdh_version",
            "fdh_fp64_peak_tflops"]
 
 
@@ -40,7 +40,7 @@ class FdhStats(C.Structure):
                 ("phase_ms", C.c_double * 8), ("apply_ms", C.c_double), ("setup_ms", C.c_double),
                 ("gpu_launches", C.c_int64), ("m2l_flops_executed", C.c_int64), ("m2l_gemm_ms", C.c_double),
                 ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
-                ("m2l_chunk", C.c_int64)]
+                ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double)]
 
 
 class FdhError(RuntimeError):
@@ -81,7 +81,7 @@ def lib():
         for f in ("fdh_export_tree", "fdh_export_perm", "fdh_export_dirsets"):
             getattr(L, f).argtypes = [C.c_void_p, C.c_int, _i64]
             getattr(L, f).restype = C.c_int64
-        for f in ("fdh_export_lplus", "fdh_export_lminus"):
+        for f in ("fdh_export_lplus", "fdh_export_lminus", "fdh_export_owned_leaves"):
             getattr(L, f).argtypes = [C.c_void_p, _i64]
             getattr(L, f).restype = C.c_int64
         L.fdh_destroy.argtypes = [C.c_void_p]
@@ -194,6 +194,9 @@ class DirectionalOperator:
 
     def dirsets(self, which):
         return self._export(lib().fdh_export_dirsets, 6, which)
+
+    def owned_leaves(self):
+        return self._export(lib().fdh_export_owned_leaves, 6)
 
 
 def version() -> str:

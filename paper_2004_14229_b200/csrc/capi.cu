@@ -510,6 +510,8 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->m2l_tiles = (int64_t)P.tile_level.size();
   s->m2l_items = (int64_t)P.item_tile.size();
   s->m2l_chunk = P.m2l_chunk;
+  s->shard_cost = P.shard_cost;
+  s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;  // DMMA issued
   return FDH_OK;
 }
@@ -525,5 +527,7 @@ int64_t fdh_export_lminus(const fdh_op* o, int64_t* rows) { return o ? export_lm
 int64_t fdh_export_dirsets(const fdh_op* o, int which, int64_t* rows) {
   return o ? export_dirsets(o->P, which, rows) : -1;
 }
+
+int64_t fdh_export_owned_leaves(const fdh_op* o, int64_t* rows) { return o ? export_owned_leaves(o->P, rows) : -1; }
 
 }  // extern "C"

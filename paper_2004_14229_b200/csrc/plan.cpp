@@ -390,6 +390,7 @@ void build_worklists(Plan& P) {
       const int32_t par = L.parent[i];
       const int oct = 4 * (int)(L.ci[i] & 1) + 2 * (int)(L.cj[i] & 1) + (int)(L.ck[i] & 1);
       (void)LP;
+      if (!P.t_needed.empty() && !P.t_needed[l + 1][i]) continue;
       for (int cc = 0; cc < T.ndir[l + 1]; ++cc) {
         const int32_t csl = slot_at(T, l + 1, (int32_t)i, cc);
         if (csl < 0) continue;
@@ -516,10 +517,11 @@ void build_m2l(Plan& P) {
     std::sort(v.begin(), v.end());
     for (int64_t i = b; i < e; ++i) { sk[i] = v[i - b].first; ss[i] = v[i - b].second; }
   }
-  // group target slots
+  // group target slots (a shard keeps only the slots of its leaves' ancestor closure)
   std::vector<int32_t> ts;
   for (int64_t t = 0; t < T.nslots; ++t)
-    if (ptr[t + 1] > ptr[t]) ts.push_back((int32_t)t);
+    if (ptr[t + 1] > ptr[t] && (P.t_needed.empty() || P.t_needed[T.slot_level[t]][T.slot_node[t]]))
+      ts.push_back((int32_t)t);
   auto gkey = [&](int32_t t) {
     const int l = T.slot_level[t];
     const int32_t nd = T.slot_node[t];
@@ -762,40 +764,80 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
         }
     }
   }
-  // ownership of target leaves (Morton-contiguous, cost-balanced) for sharded runs
+  // ownership of target leaves for sharded runs: leaves in
+  // Morton order, split into `world` contiguous ranges of equal estimated cost,
+  // cost(leaf) = sum over the leaf and its ancestors a of
+  //   (8 n^2 * #L+(a) + 24 * near-field pairs(a)) * points(leaf) / points(a).
   if (prm.world > 1) {
-    std::vector<double> cost;
-    // cost of a leaf: near-field pairs * 24 + its share of M2L over its ancestors (by points)
-    // computed after work lists would be circular; use points * (near sources) proxy below.
-    int64_t nl = 0;
-    for (int l = 0; l <= P.T.depth; ++l)
-      for (size_t i = 0; i < P.T.lv[l].size(); ++i) nl += P.T.lv[l].leaf[i];
-    // leaves in Morton order over all levels: order by (coordinate scaled to the deepest level)
+    const TreePlan& T = P.T;
+    const int D = T.depth;
+    std::vector<std::vector<double>> own(D + 1);
+    for (int l = 0; l <= D; ++l) own[l].assign(T.lv[l].size(), 0.0);
+    const double fl_m2l = 8.0 * P.n * P.n;
+    for (int l = 0; l < (int)P.blocks.size(); ++l) {
+      const LevelBlocks& B = P.blocks[l];
+      for (size_t b = 0; b < B.lp_t.size(); ++b) own[l][B.lp_t[b]] += fl_m2l;
+      for (size_t b = 0; b < B.lm_t.size(); ++b)
+        own[l][B.lm_t[b]] += 24.0 * (double)(T.lv[l].end[B.lm_t[b]] - T.lv[l].begin[B.lm_t[b]]) *
+                             (double)(P.S.lv[l].end[B.lm_s[b]] - P.S.lv[l].begin[B.lm_s[b]]);
+    }
+    // push ancestor cost down by point share: dens[l][i] = cost per point inherited
+    std::vector<std::vector<double>> dens(D + 1);
+    for (int l = 0; l <= D; ++l) {
+      dens[l].assign(T.lv[l].size(), 0.0);
+      for (size_t i = 0; i < T.lv[l].size(); ++i) {
+        const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
+        const double inh = l > 0 ? dens[l - 1][T.lv[l].parent[i]] : 0.0;
+        dens[l][i] = inh + own[l][i] / pts;
+      }
+    }
     struct LeafRef { uint64_t key; int64_t id; double c; };
     std::vector<LeafRef> lr;
     int64_t id = 0;
-    const int D = P.T.depth;
-    std::vector<double> nearcnt;
     for (int l = 0; l <= D; ++l)
-      for (size_t i = 0; i < P.T.lv[l].size(); ++i) {
-        if (!P.T.lv[l].leaf[i]) continue;
+      for (size_t i = 0; i < T.lv[l].size(); ++i) {
+        if (!T.lv[l].leaf[i]) continue;
         uint64_t k = 0;
-        const int64_t ci = P.T.lv[l].ci[i] << (D - l), cj = P.T.lv[l].cj[i] << (D - l),
-                      ck = P.T.lv[l].ck[i] << (D - l);
-        for (int b = D - 1; b >= 0; --b) k = (k << 3) | (((ci >> b) & 1) << 2) | (((cj >> b) & 1) << 1) | ((ck >> b) & 1);
-        lr.push_back({k, id++, (double)(P.T.lv[l].end[i] - P.T.lv[l].begin[i]) + 1.0});
+        const int64_t ci = T.lv[l].ci[i] << (D - l), cj = T.lv[l].cj[i] << (D - l), ck = T.lv[l].ck[i] << (D - l);
+        for (int b = D - 1; b >= 0; --b)
+          k = (k << 3) | (((ci >> b) & 1) << 2) | (((cj >> b) & 1) << 1) | ((ck >> b) & 1);
+        const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
+        lr.push_back({k, id++, dens[l][i] * pts + 1.0});
       }
     std::sort(lr.begin(), lr.end(), [](const LeafRef& a, const LeafRef& b) { return a.key < b.key; });
     double tot = 0;
     for (auto& r : lr) tot += r.c;
-    P.t_leaf_owned.assign(nl, 0);
+    P.t_leaf_owned.assign(id, 0);
+    P.shard_cost = 0.0;
     double acc = 0;
     for (auto& r : lr) {
       const double mid = acc + 0.5 * r.c;
       const int owner = std::min(prm.world - 1, (int)(mid / tot * prm.world));
-      if (owner == prm.rank) P.t_leaf_owned[r.id] = 1;
+      if (owner == prm.rank) {
+        P.t_leaf_owned[r.id] = 1;
+        P.shard_cost += r.c;
+      }
       acc += r.c;
     }
+    P.total_cost = tot;
+  }
+  if (!P.t_leaf_owned.empty()) {
+    // ancestor closure of the owned leaves (leaf ids in (level, Morton) order)
+    P.t_needed.assign(P.T.depth + 1, {});
+    for (int l = 0; l <= P.T.depth; ++l) P.t_needed[l].assign(P.T.lv[l].size(), 0);
+    int64_t lid = 0;
+    for (int l = 0; l <= P.T.depth; ++l)
+      for (size_t i = 0; i < P.T.lv[l].size(); ++i) {
+        if (!P.T.lv[l].leaf[i]) continue;
+        if (P.t_leaf_owned[lid++]) {
+          int32_t id = (int32_t)i;
+          for (int ll = l; ll >= 0 && !P.t_needed[ll][id]; --ll) {
+            P.t_needed[ll][id] = 1;
+            id = P.T.lv[ll].parent[id];
+            if (id < 0) break;
+          }
+        }
+      }
   }
   build_worklists(P);
   build_m2l(P);
@@ -889,6 +931,17 @@ int64_t export_lminus(const Plan& P, int64_t* rows) {
   std::memcpy(rows, r.data(), sizeof(int64_t) * 8 * n);
   return n;
 }
+int64_t export_owned_leaves(const Plan& P, int64_t* rows) {
+  int64_t n = (int64_t)P.l2t_level.size();
+  if (!rows) return n;
+  std::vector<std::array<int64_t, 6>> r(n);
+  for (int64_t i = 0; i < n; ++i)
+    r[i] = {P.l2t_level[i], P.l2t_ci[i], P.l2t_cj[i], P.l2t_ck[i], P.l2t_begin[i], P.l2t_end[i]};
+  std::sort(r.begin(), r.end());
+  std::memcpy(rows, r.data(), sizeof(int64_t) * 6 * n);
+  return n;
+}
+
 int64_t export_dirsets(const Plan& P, int which, int64_t* rows) {
   const TreePlan& T = which == 0 ? P.T : P.S;
   if (!rows) return T.nslots;

@@ -118,6 +118,8 @@ struct Plan {
   std::vector<int32_t> m2l_zero_slots;
   // rank ownership of targets (all by default)
   std::vector<uint8_t> t_leaf_owned;
+  std::vector<std::vector<uint8_t>> t_needed;  // [level][node]: owned leaf or ancestor of one
+  double shard_cost = 0.0, total_cost = 0.0;     // estimated flops of this shard / of all targets
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
@@ -135,6 +137,7 @@ int64_t export_perm(const TreePlan& T, int64_t* out);
 int64_t export_lplus(const Plan& P, int64_t* rows);
 int64_t export_lminus(const Plan& P, int64_t* rows);
 int64_t export_dirsets(const Plan& P, int which, int64_t* rows);
+int64_t export_owned_leaves(const Plan& P, int64_t* rows);
 
 // direction conventions
 int num_dirs(int level, int lhf);

@@ -122,3 +122,14 @@ def test_cfg2_sampled_oracle():
     err = oracle.rel_l2(y[rows], ys)
     print("cfg2 sampled rel l2", err, "rows", len(rows))
     assert err <= TOL
+
+
+def test_cpp_host_demo():
+    """The C++ host API (include/fdhelm_b200.hpp) end to end: examples/matvec_demo."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "matvec_demo")
+    out = subprocess.run([exe, "20000", "8", "4"], capture_output=True, text=True, timeout=300)
+    print(out.stdout, out.stderr)
+    assert out.returncode == 0
