@@ -315,7 +315,8 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   L += o->n_leaf > 0;
   rec(o, FDH_PHASE_P2P, st);
   launch_p2p(st, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
-             o->tz, o->sx, o->sy, o->sz, o->q, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->yslot, o->flag);
+             o->tz, o->sx, o->sy, o->sz, o->q, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->yslot, o->flag,
+             o->kappa * P.T.diam[0] * 2.0);
   L += o->n_leaf > 0;
   rec(o, FDH_PHASE_D2H, st);
   launch_scatter_y(st, o->nt, o->perm_t, o->yslot, y);

@@ -1,0 +1,76 @@
+#!/usr/bin/env python3
+"""Summarise an ncu report (--set full) or a launch-list CSV into profiles/.
+
+  python tools/ncu_summary.py report gpurun_out/prof.ncu-rep profiles/<name>.json
+  python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/<name>.json
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+    "dram__bytes_read.sum.per_second", "l1tex__t_sector_hit_rate.pct",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+]
+
+
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    kernels = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        ent = {"kernel": d.get("Kernel Name", "")[:120]}
+        for k in KEYS:
+            if k in d:
+                v = d[k].replace(",", "")
+                try:
+                    v = float(v)
+                except ValueError:
+                    pass
+                ent[k] = {"value": v, "unit": u.get(k, "")}
+        kernels.append(ent)
+    return {"source": path, "kernels": kernels}
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    agg = {}
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        k = d["Kernel Name"].split("(")[0]
+        agg.setdefault(k, []).append(float(d["Metric Value"].replace(",", "")))
+    tot = sum(sum(v) for v in agg.values())
+    ks = sorted(agg.items(), key=lambda x: -sum(x[1]))
+    return {"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none: cold-cache, serialised",
+            "kernels": [{"kernel": k, "launches": len(v), "total_ms": sum(v) / 1e6, "avg_ms": sum(v) / len(v) / 1e6,
+                         "share": sum(v) / tot} for k, v in ks]}
+
+
+if __name__ == "__main__":
+    kind, src, dst = sys.argv[1:4]
+    res = report(src) if kind == "report" else launches(src)
+    json.dump(res, open(dst, "w"), indent=1)
+    print(json.dumps(res, indent=1)[:3000])
