@@ -63,12 +63,14 @@ struct fdh_op {
   // M2L
   int n_item = 0, n_tile = 0;
   uint8_t* tile_mask = nullptr;
-  int32_t *item_tile = nullptr, *tile_keys = nullptr, *tile_src = nullptr, *tile_iptr = nullptr,
-          *tile_items = nullptr, *tile_tslot = nullptr;
+  int32_t *item_tile = nullptr, *item_seq = nullptr, *tile_keys = nullptr, *tile_src = nullptr,
+          *tile_nitem = nullptr, *tile_tslot = nullptr;
+  double* tile_acc = nullptr;
+  int* ticket = nullptr;
   int64_t *item_k0 = nullptr, *item_k1 = nullptr;
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
-  double *W = nullptr, *mom = nullptr, *loc = nullptr, *partial = nullptr;
+  double *W = nullptr, *mom = nullptr, *loc = nullptr;
   double2 *q = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
   int* flag = nullptr;
   bool timing = false;
@@ -223,13 +225,13 @@ void setup_device(fdh_op* o) {
   o->n_item = (int)P.item_tile.size();
   o->n_tile = (int)P.tile_level.size();
   o->item_tile = o->up(P.item_tile);
+  o->item_seq = o->up(P.item_seq);
   o->item_k0 = o->up(P.item_k0);
   o->item_k1 = o->up(P.item_k1);
   o->tile_keys = o->up(P.tile_keys);
   o->tile_src = o->up(P.tile_src);
   o->tile_mask = o->up(P.tile_mask);
-  o->tile_iptr = o->up(P.tile_iptr);
-  o->tile_items = o->up(P.tile_items);
+  o->tile_nitem = o->up(P.tile_nitem);
   o->tile_tslot = o->up(P.tile_tslot);
   o->key_level = o->up(P.key_level);
   o->key_dir = o->up(P.key_dir);
@@ -247,7 +249,8 @@ void setup_device(fdh_op* o) {
   o->W = o->alloc<double>((size_t)(nkeys * P.n_pad * np2));
   o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
   o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
-  o->partial = o->alloc<double>((size_t)((int64_t)o->n_item * P.n_pad * 2 * P.prm.tile));
+  o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
+  o->ticket = o->alloc<int>((size_t)std::max(o->n_tile, 1));
   o->q = o->alloc<double2>((size_t)o->ns);
   o->yslot = o->alloc<double2>((size_t)o->nt);
   o->xin = o->alloc<double2>((size_t)o->ns);
@@ -292,14 +295,28 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   rec(o, FDH_PHASE_M2L, st);
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(P.T.nslots * 2 * np), st));
   if (o->n_item > 0) {
+    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
+    M2LArgs a;
+    a.n_item = o->n_item;
+    a.item_tile = o->item_tile;
+    a.item_seq = o->item_seq;
+    a.item_k0 = o->item_k0;
+    a.item_k1 = o->item_k1;
+    a.tile_nitem = o->tile_nitem;
+    a.tile_tslot = o->tile_tslot;
+    a.tile_keys = o->tile_keys;
+    a.tile_src = o->tile_src;
+    a.tile_mask = o->tile_mask;
+    a.W = o->W;
+    a.mom = o->mom;
+    a.tile_acc = o->tile_acc;
+    a.ticket = o->ticket;
+    a.loc = o->loc;
+    a.err = o->flag;
     rec(o, FDH_NPHASES + 1, st);
-    if (launch_m2l_gemm(st, np, P.prm.tile, o->n_item, o->item_tile, o->item_k0, o->item_k1, o->tile_keys,
-                        o->tile_src, o->tile_mask, o->W, o->mom, o->partial) != 0)
-      throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+    if (launch_m2l_gemm(st, np, P.prm.tile, a) != 0) throw PlanError{4, "no M2L kernel for this n_pad / tile"};
     rec(o, FDH_NPHASES + 2, st);
-    launch_m2l_reduce(st, np, P.prm.tile, o->n_tile, o->tile_iptr, o->tile_items, o->tile_tslot, o->partial,
-                      o->loc);
-    L += 2;
+    L += 1;
   }
   rec(o, FDH_PHASE_L2L, st);
   for (int l = 0; l < (int)o->l2l.size(); ++l) {
@@ -454,7 +471,8 @@ int fdh_apply(fdh_op* o, const double* x, double* y) {
     CK(cudaMemcpyAsync(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost, o->st));
     CK(cudaStreamSynchronize(o->st));
     collect_times(o);
-    if (flag) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+    if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
+    if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
   });
 }
 

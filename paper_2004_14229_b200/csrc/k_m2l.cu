@@ -14,9 +14,9 @@
 // sm_100a (tcgen05 has no f64 kind).  Each warp owns 32 rows x 2T columns in
 // registers; A fragments stream from L2 straight into registers (no reuse
 // across warps), the gathered moments are staged once per key in shared
-// memory (cp.async, double-buffered) and shared by all warps.  Split-K over the
-// key list gives work items; partial sums are reduced in a fixed order
-// (deterministic, no atomics).
+// memory (cp.async) and shared by all warps.  Work items (tile, key chunk) run
+// chunk-major for L2 reuse of the coupling matrices; the items of a tile are
+// chained in chunk order (deterministic, no FP atomics).
 #include "kernels.hpp"
 
 namespace fdhelm {
@@ -95,7 +95,8 @@ struct M2LShape {
   static constexpr int NT = 2 * TT / 8;     // 8-column n-tiles per warp
   static constexpr int THREADS = NPAD;      // one warp per 32 rows
   static constexpr int STAGE = TT * MS;     // doubles per smem stage
-  static constexpr size_t SMEM = 2 * STAGE * sizeof(double);
+  static constexpr int NBUF = NPAD <= 128 ? 2 : 1;  // double-buffer only while 2+ CTAs/SM still fit
+  static constexpr size_t SMEM = NBUF * STAGE * sizeof(double);
 };
 
 template <int NPAD, int TT>
@@ -157,15 +158,35 @@ __device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, TT>::NT]
   }
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One work item = (tile, key chunk).  Items run chunk-major (all tiles of
+// chunk c before chunk c+1), so the coupling matrices of one chunk are shared
+// through L2 by every tile.  The items of a tile are chained in chunk order by
+// a ticket: item seq adds its register tile into the tile accumulator after
+// item seq-1 has released it (earlier items are dispatched first, so the wait
+// is short and cannot deadlock); the last item writes the locals.  Summation
+// order is fixed -> bitwise deterministic.
 template <int NPAD, int TT>
 __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ item_tile,
+                                                   const int32_t* __restrict__ item_seq,
                                                    const int64_t* __restrict__ item_k0,
                                                    const int64_t* __restrict__ item_k1,
+                                                   const int32_t* __restrict__ tile_nitem,
+                                                   const int32_t* __restrict__ tile_tslot,
                                                    const int32_t* __restrict__ tile_keys,
                                                    const int32_t* __restrict__ tile_src,
                                                    const uint8_t* __restrict__ tile_mask,
                                                    const double* __restrict__ W, const double* __restrict__ mom,
-                                                   double* __restrict__ partial) {
+                                                   double* __restrict__ tile_acc, int* __restrict__ ticket,
+                                                   double* __restrict__ loc, int* __restrict__ err) {
   using S = M2LShape<NPAD, TT>;
   constexpr int NT = S::NT;
   static_assert(NT <= 8, "mask has 8 bits");
@@ -173,7 +194,6 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x;
   const int64_t k0 = item_k0[item], k1 = item_k1[item];
-  (void)item_tile;
 
   double acc[4][NT][2];
 #pragma unroll
@@ -195,9 +215,13 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
   cp_async_commit();
   int stage = 0;
   for (int64_t kk = k0; kk < k1; ++kk) {
-    if (kk + 1 < k1) m2l_stage<NPAD, TT>(smem + (stage ^ 1) * S::STAGE, tile_src + (kk + 1) * TT, mom);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (S::NBUF == 2) {
+      if (kk + 1 < k1) m2l_stage<NPAD, TT>(smem + (stage ^ 1) * S::STAGE, tile_src + (kk + 1) * TT, mom);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
     const double* __restrict__ Wk =
         W + (int64_t)tile_keys[kk] * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
@@ -218,50 +242,72 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
       default: m2l_key<NPAD, TT, 0xF>(acc, Wk, Bs, re_off, im_off, sgn); break;
     }
     __syncthreads();
-    stage ^= 1;
+    if constexpr (S::NBUF == 2) {
+      stage ^= 1;
+    } else {
+      if (kk + 1 < k1) m2l_stage<NPAD, TT>(smem, tile_src + (kk + 1) * TT, mom);
+      cp_async_commit();
+    }
   }
-  double* P = partial + (int64_t)item * NPAD * 2 * TT;
+  // ---- chained accumulation into the tile (chunk order)
+  const int tile = item_tile[item], seq = item_seq[item], nit = tile_nitem[tile];
+  double* A = tile_acc + (int64_t)tile * NPAD * 2 * TT;
+  if (seq > 0) {
+    if (threadIdx.x == 0) {
+      long long spins = 0;
+      while (ld_acquire(ticket + tile) != seq) {
+        __nanosleep(200);
+        if (++spins > (1ll << 26)) {  // > ~10 s: report instead of hanging
+          atomicOr(err, 2);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const bool last = seq == nit - 1;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int row = warp * 32 + mt * 8 + (lane >> 2);
       const int col = nt * 8 + 2 * (lane & 3);
-      *reinterpret_cast<double2*>(P + (int64_t)row * 2 * TT + col) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      double2 v = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      double2* pa = reinterpret_cast<double2*>(A + (int64_t)row * 2 * TT + col);
+      if (seq > 0) {
+        const double2 o = __ldcg(pa);
+        v.x = o.x + v.x;
+        v.y = o.y + v.y;
+      }
+      if (last) {
+        const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
+        if (ts >= 0) {
+          loc[(int64_t)ts * 2 * NPAD + row] = v.x;          // Re(A v) (column 2j)
+          loc[(int64_t)ts * 2 * NPAD + NPAD + row] = v.y;   // Im(A v) (column 2j+1)
+        }
+      } else {
+        __stcg(pa, v);
+      }
     }
-}
-
-// Sum the partials of each tile's work items in item order and store the
-// locals of its target slots (planar re | im).
-template <int NPAD, int TT>
-__global__ void __launch_bounds__(256) k_m2l_reduce(const int32_t* __restrict__ tile_iptr,
-                                                    const int32_t* __restrict__ tile_items,
-                                                    const int32_t* __restrict__ tile_tslot,
-                                                    const double* __restrict__ partial, double* __restrict__ loc) {
-  const int tile = blockIdx.x;
-  const int i0 = tile_iptr[tile], i1 = tile_iptr[tile + 1];
-  for (int idx = threadIdx.x; idx < NPAD * 2 * TT; idx += blockDim.x) {
-    const int row = idx / (2 * TT), col = idx % (2 * TT);
-    const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
-    if (ts < 0) continue;
-    double s = 0.0;
-    for (int i = i0; i < i1; ++i) s += partial[(int64_t)tile_items[i] * NPAD * 2 * TT + idx];
-    loc[(int64_t)ts * 2 * NPAD + ((col & 1) ? NPAD : 0) + row] = s;
+  if (!last) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(ticket + tile, seq + 1);
   }
 }
 
 template <int NPAD, int TT>
-void run_gemm(cudaStream_t st, int n_item, const int32_t* item_tile, const int64_t* item_k0, const int64_t* item_k1,
-              const int32_t* tile_keys, const int32_t* tile_src, const uint8_t* tile_mask, const double* W,
-              const double* mom, double* partial) {
+void run_gemm(cudaStream_t st, const M2LArgs& a) {
   using S = M2LShape<NPAD, TT>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_m2l_gemm<NPAD, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
     attr = true;
   }
-  k_m2l_gemm<NPAD, TT><<<n_item, S::THREADS, S::SMEM, st>>>(item_tile, item_k0, item_k1, tile_keys, tile_src,
-                                                            tile_mask, W, mom, partial);
+  k_m2l_gemm<NPAD, TT><<<a.n_item, S::THREADS, S::SMEM, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1,
+                                                              a.tile_nitem, a.tile_tslot, a.tile_keys, a.tile_src,
+                                                              a.tile_mask, a.W, a.mom, a.tile_acc, a.ticket, a.loc,
+                                                              a.err);
 }
 
 }  // namespace
@@ -274,34 +320,18 @@ void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int
   k_coupling<<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, W, n, n_pad);
 }
 
-int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, int n_item, const int32_t* item_tile,
-                    const int64_t* item_k0, const int64_t* item_k1, const int32_t* tile_keys,
-                    const int32_t* tile_src, const uint8_t* tile_mask, const double* W, const double* mom,
-                    double* partial) {
-  if (n_item <= 0) return 0;
+int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, const M2LArgs& a) {
+  if (a.n_item <= 0) return 0;
   if (tile != 16) return 1;
   switch (n_pad) {
-    case 32: run_gemm<32, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
-    case 64: run_gemm<64, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
-    case 128: run_gemm<128, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
-    case 224: run_gemm<224, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
-    case 352: run_gemm<352, 16>(st, n_item, item_tile, item_k0, item_k1, tile_keys, tile_src, tile_mask, W, mom, partial); break;
+    case 32: run_gemm<32, 16>(st, a); break;
+    case 64: run_gemm<64, 16>(st, a); break;
+    case 128: run_gemm<128, 16>(st, a); break;
+    case 224: run_gemm<224, 16>(st, a); break;
+    case 352: run_gemm<352, 16>(st, a); break;
     default: return 1;
   }
   return 0;
-}
-
-void launch_m2l_reduce(cudaStream_t st, int n_pad, int tile, int n_tile, const int32_t* tile_iptr,
-                       const int32_t* tile_items, const int32_t* tile_tslot, const double* partial, double* loc) {
-  if (n_tile <= 0 || tile != 16) return;
-  switch (n_pad) {
-    case 32: k_m2l_reduce<32, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
-    case 64: k_m2l_reduce<64, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
-    case 128: k_m2l_reduce<128, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
-    case 224: k_m2l_reduce<224, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
-    case 352: k_m2l_reduce<352, 16><<<n_tile, 256, 0, st>>>(tile_iptr, tile_items, tile_tslot, partial, loc); break;
-    default: break;
-  }
 }
 
 }  // namespace fdhelm

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <unordered_map>
@@ -599,24 +600,13 @@ void build_m2l(Plan& P) {
   P.m2l_cols_exec = exec;
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
   // flight at any moment all work inside ~one chunk of key ids, so each
-  // coupling matrix is read from HBM about once per chunk and then served from
-  // L2 to every tile that uses it.  Chunk width: ~24 MB of coupling matrices,
-  // widened while the partial sums (one n_pad x 2T block per item) exceed 1.5 GB.
+  // coupling matrix is read from HBM about once and then served from L2 to
+  // every tile that uses it.  Chunk width: ~24 MB of coupling matrices.  The
+  // items of one tile are chained in chunk order (item_seq) by the kernel.
   const int64_t wbytes = (int64_t)P.n_pad * 2 * P.n_pad * 8;
-  const int64_t pbytes = (int64_t)P.n_pad * 2 * TT * 8;
-  auto count_items = [&](int64_t w) {
-    int64_t it = 0;
-    for (int64_t tl = 0; tl < ntile; ++tl) {
-      int64_t last = -1;
-      for (int64_t j = P.tile_kptr[tl]; j < P.tile_kptr[tl + 1]; ++j) {
-        const int64_t c = P.tile_keys[j] / w;
-        if (c != last) { ++it; last = c; }
-      }
-    }
-    return it;
-  };
-  int64_t cw = std::max<int64_t>(1, (int64_t)(24ll << 20) / wbytes);
-  while (cw < (int64_t)P.n_sc && count_items(cw) * pbytes > (1536ll << 20)) cw *= 2;
+  int64_t chunk_mb = 24;
+  if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
+  const int64_t cw = std::max<int64_t>(1, (chunk_mb << 20) / wbytes);
   P.m2l_chunk = cw;
   std::vector<std::array<int64_t, 4>> items;  // chunk, tile, k0, k1
   for (int64_t tl = 0; tl < ntile; ++tl) {
@@ -632,20 +622,16 @@ void build_m2l(Plan& P) {
   }
   std::sort(items.begin(), items.end());
   P.item_tile.resize(items.size());
+  P.item_seq.resize(items.size());
   P.item_k0.resize(items.size());
   P.item_k1.resize(items.size());
-  P.tile_iptr.assign(ntile + 1, 0);
+  P.tile_nitem.assign(ntile, 0);
   for (size_t i = 0; i < items.size(); ++i) {
-    P.item_tile[i] = (int32_t)items[i][1];
+    const int64_t tl = items[i][1];
+    P.item_tile[i] = (int32_t)tl;
+    P.item_seq[i] = P.tile_nitem[tl]++;
     P.item_k0[i] = items[i][2];
     P.item_k1[i] = items[i][3];
-    P.tile_iptr[items[i][1] + 1]++;
-  }
-  for (int64_t tl = 0; tl < ntile; ++tl) P.tile_iptr[tl + 1] += P.tile_iptr[tl];
-  P.tile_items.assign(items.size(), 0);
-  {
-    std::vector<int64_t> cur(P.tile_iptr.begin(), P.tile_iptr.end() - 1);
-    for (size_t i = 0; i < items.size(); ++i) P.tile_items[cur[items[i][1]]++] = (int32_t)i;  // chunk order
   }
   // target slots with no M2L contribution
   for (int64_t t = 0; t < T.nslots; ++t)

@@ -109,10 +109,10 @@ struct Plan {
   std::vector<int32_t> tile_keys;    // key ids
   std::vector<int32_t> tile_src;     // (tile_kptr[i] + kk) * T + col -> source slot or -1
   std::vector<uint8_t> tile_mask;    // per (tile, key): bit g set if columns 4g..4g+3 are not all empty
-  // work items (tile, key chunk), chunk-major; per tile CSR of its items in chunk order
-  std::vector<int32_t> item_tile;
+  // work items (tile, key chunk), chunk-major; item_seq = rank of the item in its tile
+  std::vector<int32_t> item_tile, item_seq;
   std::vector<int64_t> item_k0, item_k1;
-  std::vector<int32_t> tile_iptr, tile_items;
+  std::vector<int32_t> tile_nitem;
   int64_t m2l_chunk = 0;
   // target slots without any M2L contribution (to be zeroed)
   std::vector<int32_t> m2l_zero_slots;
