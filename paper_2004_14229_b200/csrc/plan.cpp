@@ -601,12 +601,12 @@ void build_m2l(Plan& P) {
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
   // flight at any moment all work inside ~one chunk of key ids, so each
   // coupling matrix is read from HBM about once and then served from L2 to
-  // every tile that uses it.  Chunk width: ~24 MB of coupling matrices.  The
+  // every tile that uses it.  Chunk width: ~12 MB of coupling matrices.  The
   // items of one tile are chained in chunk order (item_seq) by the kernel.
   const int64_t wbytes = (int64_t)P.n_pad * 2 * P.n_pad * 8;
-  int64_t chunk_mb = 24;
+  int64_t chunk_mb = 12;  // measured optimum 8-12 MB on config 2 (profiles/r01_m2l_chunk_sweep.txt)
   if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
-  const int64_t cw = std::max<int64_t>(1, (chunk_mb << 20) / wbytes);
+  const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
   P.m2l_chunk = cw;
   std::vector<std::array<int64_t, 4>> items;  // chunk, tile, k0, k1
   for (int64_t tl = 0; tl < ntile; ++tl) {
