@@ -82,6 +82,8 @@ typedef struct fdh_stats {
   int64_t m2l_tiles, m2l_items;  /* M2L target tiles / (tile, key chunk) items */
   int64_t m2l_chunk;            /* key ids per chunk                          */
   double shard_cost, total_cost; /* estimated flops: this shard / all targets */
+  double structure_ms;          /* trees + partition + directions + slots     */
+  int64_t gpu_structure;        /* 1: built by the k_setup.cu kernels         */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

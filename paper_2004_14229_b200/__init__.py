@@ -40,7 +40,8 @@ class FdhStats(C.Structure):
                 ("phase_ms", C.c_double * 8), ("apply_ms", C.c_double), ("setup_ms", C.c_double),
                 ("gpu_launches", C.c_int64), ("m2l_flops_executed", C.c_int64), ("m2l_gemm_ms", C.c_double),
                 ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
-                ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double)]
+                ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
+                ("structure_ms", C.c_double), ("gpu_structure", C.c_int64)]
 
 
 class FdhError(RuntimeError):

@@ -4,6 +4,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -411,6 +412,8 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     prm.zero_diagonal = zero_diagonal;
     prm.rank = rank;
     prm.world = world;
+    const char* hs = std::getenv("FDH_HOST_STRUCTURE");  // testing knob: host planner for the structure
+    prm.gpu_structure = device && !(hs && hs[0] == '1');
     o->rank = rank;
     o->world = world;
     build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
@@ -530,6 +533,8 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->m2l_items = (int64_t)P.item_tile.size();
   s->m2l_chunk = P.m2l_chunk;
   s->shard_cost = P.shard_cost;
+  s->structure_ms = P.structure_ms;
+  s->gpu_structure = P.prm.gpu_structure ? 1 : 0;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;  // DMMA issued
   return FDH_OK;

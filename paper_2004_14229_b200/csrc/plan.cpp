@@ -4,6 +4,7 @@
 // use the reference's separate FP64 multiply and add (cluster_tree.cpp:73-77,
 // geometry.hpp:69-76) to be bit-exact with it.
 #include "plan.hpp"
+#include "setup_gpu.hpp"
 
 #include <omp.h>
 
@@ -702,21 +703,28 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
   P.p = prm.m + 1;
   P.n = P.p * P.p * P.p;
   P.n_pad = (P.n + 31) / 32 * 32;
-  build_tree(P.T, tx, ty, tz, nt, lo, hi, prm.n_max, prm.depth_cap);
-  build_tree(P.S, sx, sy, sz, ns, lo, hi, prm.n_max, prm.depth_cap);
-  // l_hf default
-  P.lhf = prm.l_hf;
-  if (P.lhf == -2) {
-    P.lhf = -1;
-    for (int l = 0; l <= std::min(P.T.depth, P.S.depth); ++l)
-      if (prm.kappa * std::max(P.T.diam[l], P.S.diam[l]) >= 3.0) P.lhf = l;
+  const auto t1 = std::chrono::steady_clock::now();
+  if (prm.gpu_structure) {
+    // trees, partition, key directions, D / D^ and slots on the device (k_setup.cu)
+    gpu_build_structure(P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi);
+  } else {
+    build_tree(P.T, tx, ty, tz, nt, lo, hi, prm.n_max, prm.depth_cap);
+    build_tree(P.S, sx, sy, sz, ns, lo, hi, prm.n_max, prm.depth_cap);
+    // l_hf default
+    P.lhf = prm.l_hf;
+    if (P.lhf == -2) {
+      P.lhf = -1;
+      for (int l = 0; l <= std::min(P.T.depth, P.S.depth); ++l)
+        if (prm.kappa * std::max(P.T.diam[l], P.S.diam[l]) >= 3.0) P.lhf = l;
+    }
+    const double mn = std::min({P.T.side[0][0], P.T.side[0][1], P.T.side[0][2]});
+    for (int a = 0; a < 3; ++a) P.rho[a] = P.T.side[0][a] / mn;
+    build_blocks(P);
+    build_keys(P);
+    build_dirsets(P, P.T, true);
+    build_dirsets(P, P.S, false);
   }
-  const double mn = std::min({P.T.side[0][0], P.T.side[0][1], P.T.side[0][2]});
-  for (int a = 0; a < 3; ++a) P.rho[a] = P.T.side[0][a] / mn;
-  build_blocks(P);
-  build_keys(P);
-  build_dirsets(P, P.T, true);
-  build_dirsets(P, P.S, false);
+  P.structure_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
   // direction vector tables
   const int maxl = std::max(P.T.depth, P.S.depth);
   P.dirvec.assign(maxl + 1, {});

@@ -35,6 +35,7 @@ struct PlanParams {
   int zero_diagonal = 0;
   int tile = 16;       // M2L target slots per tile
   int rank = 0, world = 1;
+  bool gpu_structure = false;  // trees / partition / directions on the device (k_setup.cu)
 };
 
 struct LevelNodes {
@@ -125,6 +126,7 @@ struct Plan {
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
   int64_t m2l_cols_exec = 0;  // executed target columns (4-column groups with any pair)
   double setup_ms = 0.0;
+  double structure_ms = 0.0;  // trees + partition + directions + slots
 };
 
 // Throws PlanError.
