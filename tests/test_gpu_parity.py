@@ -152,3 +152,24 @@ def test_full_size_sampled_oracle(cfg, nleaf):
     err = oracle.rel_l2(y[rows], ys)
     print(f"cfg{cfg} sampled rel l2 {err:.3e} rows {len(rows)}")
     assert err <= TOL
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shards_sum_to_full_apply(world):
+    """fdh_create_shard semantics on one GPU: the ranks' outputs (their targets,
+    zeros elsewhere) sum to the single-operator result (what the NCCL all-reduce
+    in bench.py computes across GPUs)."""
+    c = CONFIGS[5]
+    tg, sr, q = make_inputs(c, nt=60000, ns=30000)
+    full = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, 4, c.eta2, c.l_hf).apply(q)
+    acc = np.zeros_like(full)
+    rows = []
+    for r in range(world):
+        op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, 4, c.eta2, c.l_hf,
+                                   rank=r, world=world)
+        y = op.apply(q)
+        own = op.owned_leaves()
+        rows.append(int((own[:, 5] - own[:, 4]).sum()))
+        acc += y
+    assert sum(rows) == c.nt if False else sum(rows) == 60000
+    assert oracle.rel_l2(acc, full) <= 1e-14
