@@ -63,7 +63,7 @@ struct fdh_op {
   uint32_t *p2p_sbeg = nullptr, *p2p_send = nullptr;
   // M2L
   int n_item = 0, n_tile = 0;
-  uint8_t* tile_mask = nullptr;
+  uint8_t *tile_cols = nullptr, *tile_cnt = nullptr, *tile_same = nullptr;
   int32_t *item_tile = nullptr, *item_seq = nullptr, *tile_keys = nullptr, *tile_src = nullptr,
           *tile_nitem = nullptr, *tile_tslot = nullptr;
   double* tile_acc = nullptr;
@@ -231,7 +231,9 @@ void setup_device(fdh_op* o) {
   o->item_k1 = o->up(P.item_k1);
   o->tile_keys = o->up(P.tile_keys);
   o->tile_src = o->up(P.tile_src);
-  o->tile_mask = o->up(P.tile_mask);
+  o->tile_cols = o->up(P.tile_cols);
+  o->tile_cnt = o->up(P.tile_cnt);
+  o->tile_same = o->up(P.tile_same);
   o->tile_nitem = o->up(P.tile_nitem);
   o->tile_tslot = o->up(P.tile_tslot);
   o->key_level = o->up(P.key_level);
@@ -247,7 +249,7 @@ void setup_device(fdh_op* o) {
   }
   const int64_t np2 = 2 * (int64_t)P.n_pad;
   const int64_t nkeys = (int64_t)P.key_level.size();
-  o->W = o->alloc<double>((size_t)(nkeys * P.n_pad * np2));
+  o->W = o->alloc<double>((size_t)(nkeys * P.n_pad * 2 * (int64_t)P.n_k));
   o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
   o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
@@ -261,10 +263,10 @@ void setup_device(fdh_op* o) {
   const int64_t chunk = 4096;
   for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
     launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
-                    o->W, P.n, P.n_pad);
+                    o->W, P.n, P.n_pad, P.n_k);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(o->st));
-  if (o->n_item > 0 && (P.n_pad != 32 && P.n_pad != 64 && P.n_pad != 128 && P.n_pad != 224 && P.n_pad != 352))
+  if (o->n_item > 0 && P.prm.m > 6)
     throw PlanError{4, "interpolation degree m=" + std::to_string(P.prm.m) + " has no compiled M2L kernel"};
 }
 
@@ -307,7 +309,9 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     a.tile_tslot = o->tile_tslot;
     a.tile_keys = o->tile_keys;
     a.tile_src = o->tile_src;
-    a.tile_mask = o->tile_mask;
+    a.tile_cols = o->tile_cols;
+    a.tile_cnt = o->tile_cnt;
+    a.tile_same = o->tile_same;
     a.W = o->W;
     a.mom = o->mom;
     a.tile_acc = o->tile_acc;
@@ -315,7 +319,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     a.loc = o->loc;
     a.err = o->flag;
     rec(o, FDH_NPHASES + 1, st);
-    if (launch_m2l_gemm(st, np, P.prm.tile, a) != 0) throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+    if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, a) != 0) throw PlanError{4, "no M2L kernel for this n_pad / tile"};
     rec(o, FDH_NPHASES + 2, st);
     L += 1;
   }
@@ -536,7 +540,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->structure_ms = P.structure_ms;
   s->gpu_structure = P.prm.gpu_structure ? 1 : 0;
   s->total_cost = P.total_cost;
-  s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_pad * 2;  // DMMA issued
+  s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_k * 2;  // DMMA issued
   return FDH_OK;
 }
 

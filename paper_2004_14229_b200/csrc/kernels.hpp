@@ -34,13 +34,13 @@ void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg,
 // ---- k_m2l.cu
 void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                      const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double* W,
-                     int n, int n_pad);
+                     int n, int n_pad, int n_k);
 struct M2LArgs {
   int n_item = 0;
   const int32_t *item_tile = nullptr, *item_seq = nullptr;
   const int64_t *item_k0 = nullptr, *item_k1 = nullptr;
   const int32_t *tile_nitem = nullptr, *tile_tslot = nullptr, *tile_keys = nullptr, *tile_src = nullptr;
-  const uint8_t* tile_mask = nullptr;
+  const uint8_t *tile_cols = nullptr, *tile_cnt = nullptr, *tile_same = nullptr;
   const double *W = nullptr, *mom = nullptr;
   double* tile_acc = nullptr;
   int* ticket = nullptr;
@@ -48,6 +48,6 @@ struct M2LArgs {
   int* err = nullptr;
 };
 // returns 0 on success, nonzero if the n_pad / tile combination is not compiled
-int launch_m2l_gemm(cudaStream_t st, int n_pad, int tile, const M2LArgs& a);
+int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a);
 
 }  // namespace fdhelm

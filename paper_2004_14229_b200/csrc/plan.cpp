@@ -586,17 +586,34 @@ void build_m2l(Plan& P) {
       }
     }
   }
-  P.tile_mask.assign(tot, 0);
+  // compact the valid columns of every (tile, key) to the front
+  P.tile_cols.assign(tot * TT, 0);
+  P.tile_cnt.assign(tot, 0);
+  P.tile_same.assign(tot, 0);
   int64_t exec = 0;
-  for (int64_t i = 0; i < tot; ++i) {
-    uint8_t mk = 0;
-    for (int c = 0; c < TT; ++c)
-      if (P.tile_src[i * TT + c] >= 0) mk |= (uint8_t)(1u << (c / 4));
-    P.tile_mask[i] = mk;
-    // masks with their own kernel loop (k_m2l.cu); other masks run all 4 n-tiles
-    const bool special = mk == 0xF || mk == 0x3 || mk == 0xC || mk == 0x5 || mk == 0xA || mk == 0x1 ||
-                         mk == 0x2 || mk == 0x4 || mk == 0x8;
-    exec += special ? 4 * __builtin_popcount(mk) : 16;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : exec)
+  for (int64_t tl = 0; tl < ntile; ++tl) {
+    for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
+      int cnt = 0;
+      int32_t src[64];
+      uint8_t col[64];
+      for (int c = 0; c < TT; ++c)
+        if (P.tile_src[i * TT + c] >= 0) {
+          src[cnt] = P.tile_src[i * TT + c];
+          col[cnt] = (uint8_t)c;
+          ++cnt;
+        }
+      for (int j = 0; j < TT; ++j) {
+        P.tile_src[i * TT + j] = j < cnt ? src[j] : -1;
+        P.tile_cols[i * TT + j] = j < cnt ? col[j] : 0;
+      }
+      P.tile_cnt[i] = (uint8_t)cnt;
+      if (i > P.tile_kptr[tl] && P.tile_cnt[i - 1] == cnt &&
+          std::equal(P.tile_cols.begin() + i * TT, P.tile_cols.begin() + i * TT + cnt,
+                     P.tile_cols.begin() + (i - 1) * TT))
+        P.tile_same[i] = 1;
+      exec += 4 * ((cnt + 3) / 4);
+    }
   }
   P.m2l_cols_exec = exec;
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
@@ -604,7 +621,7 @@ void build_m2l(Plan& P) {
   // coupling matrix is read from HBM about once and then served from L2 to
   // every tile that uses it.  Chunk width: ~12 MB of coupling matrices.  The
   // items of one tile are chained in chunk order (item_seq) by the kernel.
-  const int64_t wbytes = (int64_t)P.n_pad * 2 * P.n_pad * 8;
+  const int64_t wbytes = (int64_t)P.n_pad * 2 * P.n_k * 8;
   int64_t chunk_mb = 12;  // measured optimum 8-12 MB on config 2 (profiles/r01_m2l_chunk_sweep.txt)
   if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
   const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
@@ -703,6 +720,7 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
   P.p = prm.m + 1;
   P.n = P.p * P.p * P.p;
   P.n_pad = (P.n + 31) / 32 * 32;
+  P.n_k = (P.n + 7) / 8 * 8;
   const auto t1 = std::chrono::steady_clock::now();
   if (prm.gpu_structure) {
     // trees, partition, key directions, D / D^ and slots on the device (k_setup.cu)

@@ -72,7 +72,7 @@ struct LevelBlocks {
 
 struct Plan {
   PlanParams prm;
-  int p = 0, n = 0, n_pad = 0, lhf = -1;
+  int p = 0, n = 0, n_pad = 0, n_k = 0, lhf = -1;  // n_pad: GEMM rows (32k), n_k: K half (8k)
   double rho[3] = {1, 1, 1};
   TreePlan T, S;
   std::vector<LevelBlocks> blocks;
@@ -108,8 +108,10 @@ struct Plan {
   std::vector<int32_t> tile_tslot;   // tile * T (-1 pad)
   std::vector<int64_t> tile_kptr;    // CSR into tile_keys / tile_src
   std::vector<int32_t> tile_keys;    // key ids
-  std::vector<int32_t> tile_src;     // (tile_kptr[i] + kk) * T + col -> source slot or -1
-  std::vector<uint8_t> tile_mask;    // per (tile, key): bit g set if columns 4g..4g+3 are not all empty
+  std::vector<int32_t> tile_src;     // (tile_kptr[i] + kk) * T + j: source slot of compacted column j
+  std::vector<uint8_t> tile_cols;    // (tile_kptr[i] + kk) * T + j: target column of compacted column j
+  std::vector<uint8_t> tile_cnt;     // per (tile, key): number of target columns that have the key
+  std::vector<uint8_t> tile_same;    // per (tile, key): same column map as the previous key of the tile
   // work items (tile, key chunk), chunk-major; item_seq = rank of the item in its tile
   std::vector<int32_t> item_tile, item_seq;
   std::vector<int64_t> item_k0, item_k1;
@@ -124,7 +126,7 @@ struct Plan {
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
-  int64_t m2l_cols_exec = 0;  // executed target columns (4-column groups with any pair)
+  int64_t m2l_cols_exec = 0;  // executed target columns (4 * ceil(cnt / 4) per tile key)
   double setup_ms = 0.0;
   double structure_ms = 0.0;  // trees + partition + directions + slots
 };

@@ -171,5 +171,5 @@ def test_shards_sum_to_full_apply(world):
         own = op.owned_leaves()
         rows.append(int((own[:, 5] - own[:, 4]).sum()))
         acc += y
-    assert sum(rows) == c.nt if False else sum(rows) == 60000
+    assert sum(rows) == 60000  # every target row owned by exactly one rank
     assert oracle.rel_l2(acc, full) <= 1e-14
