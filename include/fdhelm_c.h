@@ -84,6 +84,8 @@ typedef struct fdh_stats {
   double shard_cost, total_cost; /* estimated flops: this shard / all targets */
   double structure_ms;          /* trees + partition + directions + slots     */
   int64_t gpu_structure;        /* 1: built by the k_setup.cu kernels         */
+  int64_t w_resident;           /* 1: coupling matrices kept in HBM           */
+  int64_t w_segments;           /* else: per-apply generation segments        */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

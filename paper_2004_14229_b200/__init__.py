@@ -41,7 +41,8 @@ class FdhStats(C.Structure):
                 ("gpu_launches", C.c_int64), ("m2l_flops_executed", C.c_int64), ("m2l_gemm_ms", C.c_double),
                 ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
                 ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
-                ("structure_ms", C.c_double), ("gpu_structure", C.c_int64)]
+                ("structure_ms", C.c_double), ("gpu_structure", C.c_int64), ("w_resident", C.c_int64),
+                ("w_segments", C.c_int64)]
 
 
 class FdhError(RuntimeError):

@@ -72,6 +72,14 @@ struct fdh_op {
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
   double *W = nullptr, *mom = nullptr, *loc = nullptr;
+  // on-the-fly coupling (W does not fit): segments of consecutive key chunks, 2-slot ring
+  bool w_resident = true;
+  struct Seg {
+    int item0, item1;
+    int64_t key0, key1;
+  };
+  std::vector<Seg> segs;
+  int64_t w_slot_keys = 0;
   double2 *q = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
   int* flag = nullptr;
   bool timing = false;
@@ -249,7 +257,7 @@ void setup_device(fdh_op* o) {
   }
   const int64_t np2 = 2 * (int64_t)P.n_pad;
   const int64_t nkeys = (int64_t)P.key_level.size();
-  o->W = o->alloc<double>((size_t)(nkeys * P.n_pad * 2 * (int64_t)P.n_k));
+  const int64_t wkey = P.n_pad * 2 * (int64_t)P.n_k;  // doubles per coupling matrix
   o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
   o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
@@ -259,11 +267,36 @@ void setup_device(fdh_op* o) {
   o->xin = o->alloc<double2>((size_t)o->ns);
   o->yout = o->alloc<double2>((size_t)o->nt);
   o->flag = o->alloc<int>(1);
-  // coupling matrices (populated at setup), in key chunks
-  const int64_t chunk = 4096;
-  for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
-    launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
-                    o->W, P.n, P.n_pad, P.n_k);
+  // coupling matrices: resident when they fit (70 % of the free
+  // memory), else generated per apply in segments of key chunks (config 4: 240 GB)
+  size_t fre = 0, tot = 0;
+  CK(cudaMemGetInfo(&fre, &tot));
+  const double wbytes = 8.0 * (double)wkey * (double)nkeys;
+  const char* otf = std::getenv("FDH_W_ONTHEFLY");
+  o->w_resident = !(otf && otf[0] == '1') && wbytes <= 0.7 * (double)fre;
+  if (o->w_resident) {
+    o->W = o->alloc<double>((size_t)(nkeys * wkey));
+    const int64_t chunk = 4096;
+    for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+      launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
+                      o->W, P.n, P.n_pad, P.n_k, 0);
+  } else {
+    // ring of 2 slots, each ~min(8 GB, 20 % of free memory); segments = whole key chunks
+    const double slot_bytes = std::min(8.0e9, 0.2 * (double)fre);
+    int64_t slot_keys = std::max<int64_t>(P.m2l_chunk, (int64_t)(slot_bytes / (8.0 * wkey)) / P.m2l_chunk * P.m2l_chunk);
+    o->w_slot_keys = slot_keys;
+    o->W = o->alloc<double>((size_t)(2 * slot_keys * wkey));
+    // items are sorted by key chunk: cut them where the chunk crosses a slot boundary
+    const int64_t ni = (int64_t)P.item_tile.size();
+    int64_t i = 0;
+    while (i < ni) {
+      const int64_t seg = P.tile_keys[P.item_k0[i]] / slot_keys;
+      int64_t j = i;
+      while (j < ni && P.tile_keys[P.item_k0[j]] / slot_keys == seg) ++j;
+      o->segs.push_back({(int)i, (int)j, seg * slot_keys, std::min(nkeys, (seg + 1) * slot_keys)});
+      i = j;
+    }
+  }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(o->st));
   if (o->n_item > 0 && P.prm.m > 6)
@@ -319,7 +352,25 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     a.loc = o->loc;
     a.err = o->flag;
     rec(o, FDH_NPHASES + 1, st);
-    if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, a) != 0) throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+    if (o->w_resident) {
+      if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, a) != 0)
+        throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+    } else {
+      for (size_t sg = 0; sg < o->segs.size(); ++sg) {
+        const auto& S = o->segs[sg];
+        double* slot = o->W + (int64_t)(sg & 1) * o->w_slot_keys * P.n_pad * 2 * (int64_t)P.n_k;
+        launch_coupling(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, slot,
+                        P.n, P.n_pad, P.n_k, S.key0);
+        M2LArgs b = a;
+        b.item0 = S.item0;
+        b.n_item = S.item1 - S.item0;
+        b.W = slot;
+        b.key_base = S.key0;
+        if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, b) != 0)
+          throw PlanError{4, "no M2L kernel for this n_pad / tile"};
+        L += 2;
+      }
+    }
     rec(o, FDH_NPHASES + 2, st);
     L += 1;
   }
@@ -539,6 +590,8 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->shard_cost = P.shard_cost;
   s->structure_ms = P.structure_ms;
   s->gpu_structure = P.prm.gpu_structure ? 1 : 0;
+  s->w_resident = o->w_resident ? 1 : 0;
+  s->w_segments = (int64_t)o->segs.size();
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_cols_exec * 2 * (int64_t)P.n_pad * 2 * (int64_t)P.n_k * 2;  // DMMA issued
   return FDH_OK;

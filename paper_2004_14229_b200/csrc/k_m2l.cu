@@ -20,10 +20,15 @@
 // chained in chunk order (deterministic, no FP atomics).
 #include "kernels.hpp"
 
+#ifndef FDH_KUNROLL
+#define FDH_KUNROLL 4
+#endif
+
 namespace fdhelm {
 
 namespace {
 
+constexpr int kKUnroll = FDH_KUNROLL;  // k-step unroll of the DMMA loops
 constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // geometry.hpp:11
 
 // ---------------------------------------------------------- coupling gen
@@ -33,7 +38,7 @@ constexpr int kCplRows = 8;
 __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, const double* __restrict__ dirtab,
                                                   int64_t key0, const int32_t* __restrict__ key_level,
                                                   const int64_t* __restrict__ key_d, const int32_t* __restrict__ key_dir,
-                                                  double* __restrict__ W, int n, int n_pad, int n_k) {
+                                                  double* __restrict__ W, int n, int n_pad, int n_k, int64_t wbase) {
   __shared__ double tn[3][kMaxP], sn[3][kMaxP];
   const int64_t key = key0 + blockIdx.x;
   const int r0 = blockIdx.y * kCplRows;
@@ -50,7 +55,7 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
   const double cv[3] = {c[0], c[1], c[2]};
   const double kappa = C->kappa;
   __syncthreads();
-  double* Wk = W + key * n_pad * 2 * n_k;
+  double* Wk = W + (key - wbase) * n_pad * 2 * n_k;
   for (int idx = threadIdx.x; idx < kCplRows * n_k; idx += blockDim.x) {
     const int j = r0 + idx / n_k, k = idx % n_k;
     if (j >= n_pad) continue;
@@ -128,7 +133,7 @@ __device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, NK, TT>:
                                         const double* Bs, int re_off, int im_off, unsigned long long sgn) {
   using S = M2LShape<NPAD, NK, TT>;
   // K half 1: columns of Re A against (Re v, Im v)
-#pragma unroll 4
+#pragma unroll kKUnroll
   for (int ks = 0; ks < NK / 4; ++ks) {
     double a[4], b[NTA];
 #pragma unroll
@@ -141,7 +146,7 @@ __device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, NK, TT>:
       for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
   }
   // K half 2: columns of Im A against (-Im v, Re v)
-#pragma unroll 4
+#pragma unroll kKUnroll
   for (int ks = 0; ks < NK / 4; ++ks) {
     double a[4], b[NTA];
 #pragma unroll
@@ -211,14 +216,15 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
                                                    const uint8_t* __restrict__ tile_same,
                                                    const double* __restrict__ W, const double* __restrict__ mom,
                                                    double* __restrict__ tile_acc, int* __restrict__ ticket,
-                                                   double* __restrict__ loc, int* __restrict__ err) {
+                                                   double* __restrict__ loc, int* __restrict__ err, int item0,
+                                                   int64_t key_base) {
   using S = M2LShape<NPAD, NK, TT>;
   constexpr int NT = S::NT;
   static_assert(NT == 4, "one warp row-block covers 4 n-tiles");
   extern __shared__ __align__(16) double smem[];
   double* sacc = smem + S::NBUF * S::STAGE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x;
+  const int item = item0 + (int)blockIdx.x;
   const int64_t k0 = item_k0[item], k1 = item_k1[item];
 
   for (int i = threadIdx.x; i < NPAD * S::SA; i += S::THREADS) sacc[i] = 0.0;
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
     if (kk > k0 && !tile_same[kk]) m2l_flush<NPAD, NK, TT>(acc, sacc, tile_cols + (kk - 1) * TT, tile_cnt[kk - 1], warp,
                                                        lane);
     const double* __restrict__ Wk =
-        W + (int64_t)tile_keys[kk] * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
+        W + ((int64_t)tile_keys[kk] - key_base) * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
     const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
     switch ((cnt + 3) >> 2) {  // warp-uniform: only the n-tiles holding columns
       case 1: m2l_key<NPAD, NK, TT, 1>(acc, Wk, Bs, re_off, im_off, sgn); break;
@@ -336,17 +342,18 @@ void run_gemm(cudaStream_t st, const M2LArgs& a) {
   k_m2l_gemm<NPAD, NK, TT><<<a.n_item, S::THREADS, S::SMEM, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1,
                                                               a.tile_nitem, a.tile_tslot, a.tile_keys, a.tile_src,
                                                               a.tile_cols, a.tile_cnt, a.tile_same, a.W, a.mom,
-                                                              a.tile_acc, a.ticket, a.loc, a.err);
+                                                              a.tile_acc, a.ticket, a.loc, a.err, a.item0,
+                                                              a.key_base);
 }
 
 }  // namespace
 
 void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                      const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double* W, int n,
-                     int n_pad, int n_k) {
+                     int n_pad, int n_k, int64_t wbase) {
   if (nkeys <= 0) return;
   dim3 grid((unsigned)nkeys, (unsigned)((n_pad + kCplRows - 1) / kCplRows));
-  k_coupling<<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, W, n, n_pad, n_k);
+  k_coupling<<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, W, n, n_pad, n_k, wbase);
 }
 
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a) {

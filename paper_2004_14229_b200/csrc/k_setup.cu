@@ -539,25 +539,32 @@ __global__ void k_emit(int64_t np, const int32_t* __restrict__ pt, const int32_t
   }
 }
 
-// keys: offsets in a dense box [mn, mn + ext) per level
-__global__ void k_offsets(int64_t nb, const int32_t* __restrict__ lpt, const int32_t* __restrict__ lps,
-                          const int64_t* __restrict__ tci, const int64_t* __restrict__ tcj,
-                          const int64_t* __restrict__ tck, const int64_t* __restrict__ sci,
-                          const int64_t* __restrict__ scj, const int64_t* __restrict__ sck, int64_t* __restrict__ d) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= nb) return;
-  d[3 * b] = tci[lpt[b]] - sci[lps[b]];
-  d[3 * b + 1] = tcj[lpt[b]] - scj[lps[b]];
-  d[3 * b + 2] = tck[lpt[b]] - sck[lps[b]];
+// keys: lattice offsets of the L+ pairs, in a dense box [mn, mn + ext) per level
+__device__ __forceinline__ void pair_offset(int64_t b, const int32_t* __restrict__ lpt, const int32_t* __restrict__ lps,
+                                            const int64_t* __restrict__ tci, const int64_t* __restrict__ tcj,
+                                            const int64_t* __restrict__ tck, const int64_t* __restrict__ sci,
+                                            const int64_t* __restrict__ scj, const int64_t* __restrict__ sck,
+                                            long long d[3]) {
+  const int32_t t = lpt[b], s = lps[b];
+  d[0] = tci[t] - sci[s];
+  d[1] = tcj[t] - scj[s];
+  d[2] = tck[t] - sck[s];
 }
-__global__ void k_minmax(int64_t nb, const int64_t* __restrict__ d, long long* __restrict__ mm) {
+#define FDH_PAIR_ARGS                                                                                          \
+  const int32_t *__restrict__ lpt, const int32_t *__restrict__ lps, const int64_t *__restrict__ tci,          \
+      const int64_t *__restrict__ tcj, const int64_t *__restrict__ tck, const int64_t *__restrict__ sci,      \
+      const int64_t *__restrict__ scj, const int64_t *__restrict__ sck
+__global__ void k_minmax(int64_t nb, FDH_PAIR_ARGS, long long* __restrict__ mm) {
   __shared__ long long sh[6][256];
   long long v[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    long long d[3];
+    pair_offset(b, lpt, lps, tci, tcj, tck, sci, scj, sck, d);
     for (int a = 0; a < 3; ++a) {
-      v[a] = min(v[a], (long long)d[3 * b + a]);
-      v[3 + a] = max(v[3 + a], (long long)d[3 * b + a]);
+      v[a] = min(v[a], d[a]);
+      v[3 + a] = max(v[3 + a], d[a]);
     }
+  }
   for (int k = 0; k < 6; ++k) sh[k][threadIdx.x] = v[k];
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -572,18 +579,21 @@ __global__ void k_minmax(int64_t nb, const int64_t* __restrict__ d, long long* _
     }
   }
 }
-__global__ void k_mark(int64_t nb, const int64_t* __restrict__ d, long long m0, long long m1, long long m2,
-                       long long e1, long long e2, int64_t* __restrict__ tab) {
+__global__ void k_mark(int64_t nb, FDH_PAIR_ARGS, long long m0, long long m1, long long m2, long long e1,
+                       long long e2, int64_t* __restrict__ tab) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
-  tab[((d[3 * b] - m0) * e1 + (d[3 * b + 1] - m1)) * e2 + (d[3 * b + 2] - m2)] = 1;
+  long long d[3];
+  pair_offset(b, lpt, lps, tci, tcj, tck, sci, scj, sck, d);
+  tab[((d[0] - m0) * e1 + (d[1] - m1)) * e2 + (d[2] - m2)] = 1;
 }
-__global__ void k_keyids(int64_t nb, const int64_t* __restrict__ d, long long m0, long long m1, long long m2,
-                         long long e1, long long e2, const int64_t* __restrict__ tabscan, int32_t base,
-                         int32_t* __restrict__ key) {
+__global__ void k_keyids(int64_t nb, FDH_PAIR_ARGS, long long m0, long long m1, long long m2, long long e1,
+                         long long e2, const int64_t* __restrict__ tabscan, int32_t base, int32_t* __restrict__ key) {
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
-  key[b] = base + (int32_t)tabscan[((d[3 * b] - m0) * e1 + (d[3 * b + 1] - m1)) * e2 + (d[3 * b + 2] - m2)];
+  long long d[3];
+  pair_offset(b, lpt, lps, tci, tcj, tck, sci, scj, sck, d);
+  key[b] = base + (int32_t)tabscan[((d[0] - m0) * e1 + (d[1] - m1)) * e2 + (d[2] - m2)];
 }
 __global__ void k_keylist(int64_t vol, const int64_t* __restrict__ flag, const int64_t* __restrict__ tabscan,
                           long long m0, long long m1, long long m2, long long e1, long long e2,
@@ -671,7 +681,11 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
   const double mn = std::min({P.T.side[0][0], P.T.side[0][1], P.T.side[0][2]});
   for (int a = 0; a < 3; ++a) P.rho[a] = P.T.side[0][a] / mn;
 
-  // ---- block partition, level by level
+  // ---- block partition, level by level; candidate pairs in chunks of kPairChunk
+  // (two passes: counts, then scan + emit at global offsets) so the scratch of a
+  // 3e9-pair level (config 4) stays a few GB
+  int64_t kPairChunk = (int64_t)1 << 27;
+  if (const char* e = std::getenv("FDH_SETUP_PAIR_CHUNK")) kPairChunk = std::max(1024LL, std::atoll(e));  // testing
   const int maxl = std::min(P.T.depth, P.S.depth);
   P.blocks.assign(maxl + 1, {});
   int32_t* pt = D.up(std::vector<int32_t>{0});
@@ -679,7 +693,6 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
   int64_t np = 1;
   std::vector<int32_t*> lpt(maxl + 1, nullptr), lps(maxl + 1, nullptr), lpk(maxl + 1, nullptr);
   std::vector<int64_t> nlp(maxl + 1, 0);
-  std::vector<int64_t> keyd_all;  // 3 per key
   int32_t key_base = 0;
   for (int l = 0; np > 0; ++l) {
     if (l > maxl) throw PlanError{1, "internal: block recursion beyond tree depth"};
@@ -695,22 +708,50 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
     }
     const DevLevel& LT = dT[l];
     const DevLevel& LS = dS[l];
-    int64_t* olp = D.alloc<int64_t>(np);
-    int64_t* olm = D.alloc<int64_t>(np);
-    int64_t* onx = D.alloc<int64_t>(np);
-    k_classify<<<nblocks(np), 256>>>(np, pt, ps, g, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, LT.leaf, LS.leaf,
-                                     LT.child, LS.child, olp, olm, onx);
-    SCK(cudaGetLastError());
-    const int64_t tlp = scan_excl(D, olp, np), tlm = scan_excl(D, olm, np), tnx = scan_excl(D, onx, np);
+    const int64_t cap = std::min(np, kPairChunk);
+    int64_t* olp = D.alloc<int64_t>(cap);
+    int64_t* olm = D.alloc<int64_t>(cap);
+    int64_t* onx = D.alloc<int64_t>(cap);
+    // pass 1: totals per chunk
+    std::vector<std::array<int64_t, 3>> ctot;
+    for (int64_t c0 = 0; c0 < np; c0 += kPairChunk) {
+      const int64_t nc = std::min(kPairChunk, np - c0);
+      k_classify<<<nblocks(nc), 256>>>(nc, pt + c0, ps + c0, g, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, LT.leaf,
+                                       LS.leaf, LT.child, LS.child, olp, olm, onx);
+      SCK(cudaGetLastError());
+      ctot.push_back({scan_excl(D, olp, nc), scan_excl(D, olm, nc), scan_excl(D, onx, nc)});
+    }
+    int64_t tlp = 0, tlm = 0, tnx = 0;
+    for (auto& t : ctot) {
+      tlp += t[0];
+      tlm += t[1];
+      tnx += t[2];
+    }
     int32_t* a_t = D.alloc<int32_t>(tlp);
     int32_t* a_s = D.alloc<int32_t>(tlp);
     int32_t* m_t = D.alloc<int32_t>(tlm);
     int32_t* m_s = D.alloc<int32_t>(tlm);
     int32_t* n_t = D.alloc<int32_t>(tnx);
     int32_t* n_s = D.alloc<int32_t>(tnx);
-    k_emit<<<nblocks(np), 256>>>(np, pt, ps, olp, olm, onx, tlp, tlm, tnx, LT.child, LS.child, a_t, a_s, m_t, m_s,
-                                 n_t, n_s);
-    SCK(cudaGetLastError());
+    // pass 2: classify again, scan, emit at the chunk's global offsets
+    int64_t blp = 0, blm = 0, bnx = 0;
+    for (size_t ci = 0; ci * kPairChunk < (size_t)np; ++ci) {
+      const int64_t c0 = (int64_t)ci * kPairChunk, nc = std::min(kPairChunk, np - c0);
+      if (ctot.size() > 1) {
+        k_classify<<<nblocks(nc), 256>>>(nc, pt + c0, ps + c0, g, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, LT.leaf,
+                                         LS.leaf, LT.child, LS.child, olp, olm, onx);
+        scan_excl(D, olp, nc);
+        scan_excl(D, olm, nc);
+        scan_excl(D, onx, nc);
+      }
+      k_emit<<<nblocks(nc), 256>>>(nc, pt + c0, ps + c0, olp, olm, onx, ctot[ci][0], ctot[ci][1], ctot[ci][2],
+                                   LT.child, LS.child, a_t + blp, a_s + blp, m_t + blm, m_s + blm, n_t + bnx,
+                                   n_s + bnx);
+      SCK(cudaGetLastError());
+      blp += ctot[ci][0];
+      blm += ctot[ci][1];
+      bnx += ctot[ci][2];
+    }
     if (std::getenv("FDH_DEBUG_SETUP"))
       std::fprintf(stderr, "[setup] level %d: pairs %lld  L+ %lld  L- %lld  next %lld\n", l, (long long)np,
                    (long long)tlp, (long long)tlm, (long long)tnx);
@@ -720,26 +761,28 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
     lpt[l] = a_t;
     lps[l] = a_s;
     nlp[l] = tlp;
-    // keys of this level
+    for (void* p : {(void*)olp, (void*)olm, (void*)onx, (void*)m_t, (void*)m_s, (void*)pt, (void*)ps}) D.release(p);
+    // keys of this level: dense offset table, ids in (dx, dy, dz) order
     if (tlp > 0) {
-      int64_t* d = D.alloc<int64_t>(3 * tlp);
-      k_offsets<<<nblocks(tlp), 256>>>(tlp, a_t, a_s, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, d);
       long long init[6] = {LLONG_MAX, LLONG_MAX, LLONG_MAX, LLONG_MIN, LLONG_MIN, LLONG_MIN};
       long long* mm = D.alloc<long long>(6);
       SCK(cudaMemcpy(mm, init, sizeof(init), cudaMemcpyHostToDevice));
-      k_minmax<<<std::min<unsigned>(1024, nblocks(tlp)), 256>>>(tlp, d, mm);
+      k_minmax<<<std::min<unsigned>(1024, nblocks(tlp)), 256>>>(tlp, a_t, a_s, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj,
+                                                                LS.ck, mm);
       std::vector<long long> m = down(mm, 6);
       const long long e0 = m[3] - m[0] + 1, e1 = m[4] - m[1] + 1, e2 = m[5] - m[2] + 1;
       const long long vol = e0 * e1 * e2;
       if (vol > (1ll << 28)) throw PlanError{4, "lattice offset range too large for the dense key table"};
       int64_t* tab = D.alloc<int64_t>(vol);
       SCK(cudaMemset(tab, 0, vol * 8));
-      k_mark<<<nblocks(tlp), 256>>>(tlp, d, m[0], m[1], m[2], e1, e2, tab);
+      k_mark<<<nblocks(tlp), 256>>>(tlp, a_t, a_s, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, m[0], m[1], m[2], e1,
+                                    e2, tab);
       int64_t* flag = D.alloc<int64_t>(vol);
       SCK(cudaMemcpy(flag, tab, vol * 8, cudaMemcpyDeviceToDevice));
       const int64_t nk = scan_excl(D, tab, vol);
       int32_t* key = D.alloc<int32_t>(tlp);
-      k_keyids<<<nblocks(tlp), 256>>>(tlp, d, m[0], m[1], m[2], e1, e2, tab, key_base, key);
+      k_keyids<<<nblocks(tlp), 256>>>(tlp, a_t, a_s, LT.ci, LT.cj, LT.ck, LS.ci, LS.cj, LS.ck, m[0], m[1], m[2], e1,
+                                      e2, tab, key_base, key);
       int64_t* kd = D.alloc<int64_t>(3 * nk);
       k_keylist<<<nblocks(vol), 256>>>(vol, flag, tab, m[0], m[1], m[2], e1, e2, kd);
       int32_t* kdir = D.alloc<int32_t>(nk);
@@ -756,9 +799,8 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
       }
       lpk[l] = key;
       key_base += (int32_t)nk;
-      for (void* p : {(void*)d, (void*)mm, (void*)tab, (void*)flag, (void*)kd, (void*)kdir}) D.release(p);
+      for (void* p : {(void*)mm, (void*)tab, (void*)flag, (void*)kd, (void*)kdir}) D.release(p);
     }
-    for (void* p : {(void*)olp, (void*)olm, (void*)onx, (void*)m_t, (void*)m_s, (void*)pt, (void*)ps}) D.release(p);
     pt = n_t;
     ps = n_s;
     np = tnx;

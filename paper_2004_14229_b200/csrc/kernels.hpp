@@ -34,9 +34,11 @@ void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg,
 // ---- k_m2l.cu
 void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                      const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double* W,
-                     int n, int n_pad, int n_k);
+                     int n, int n_pad, int n_k, int64_t wbase);
 struct M2LArgs {
-  int n_item = 0;
+  int n_item = 0;      // items of this launch: [item0, item0 + n_item)
+  int item0 = 0;
+  int64_t key_base = 0;  // W holds the keys [key_base, ...) (on-the-fly coupling segments)
   const int32_t *item_tile = nullptr, *item_seq = nullptr;
   const int64_t *item_k0 = nullptr, *item_k1 = nullptr;
   const int32_t *tile_nitem = nullptr, *tile_tslot = nullptr, *tile_keys = nullptr, *tile_src = nullptr;

@@ -73,3 +73,11 @@ def test_gpu_structure_single_point_and_errors():
     with pytest.raises(F.FdhError) as e:
         F.DirectionalOperator(bad, bad, (0, 0, 0), (1, 1, 1), 1.0)
     assert e.value.code == F.ERR_ARG
+
+
+def test_gpu_structure_chunked_pairs(monkeypatch):
+    """the chunked two-pass partition (used for the 3e9-pair levels of config 4)"""
+    monkeypatch.setenv("FDH_SETUP_PAIR_CHUNK", "5000")
+    c = CONFIGS[2]
+    tg, sr, _ = make_inputs(c, nt=40000, ns=30000)
+    compare(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
