@@ -21,14 +21,13 @@
 #include "kernels.hpp"
 
 #ifndef FDH_KUNROLL
-#define FDH_KUNROLL 4
+#define FDH_KUNROLL 0
 #endif
 
 namespace fdhelm {
 
 namespace {
 
-constexpr int kKUnroll = FDH_KUNROLL;  // k-step unroll of the DMMA loops
 constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // geometry.hpp:11
 
 // ---------------------------------------------------------- coupling gen
@@ -72,8 +71,11 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
       re = __dmul_rn(w, co);
       im = __dmul_rn(w, s);
     }
-    Wk[(int64_t)j * 2 * n_k + k] = re;
-    Wk[(int64_t)j * 2 * n_k + n_k + k] = im;
+    // k-interleaved within blocks of 8 (k = 8b + 4h + q stored at 8b + 2q + h), so
+    // that a lane's A fragments of two consecutive k-steps are one 16-byte load
+    const int kp = (k & ~7) | ((k & 3) << 1) | ((k >> 2) & 1);
+    Wk[(int64_t)j * 2 * n_k + kp] = re;
+    Wk[(int64_t)j * 2 * n_k + n_k + kp] = im;
   }
 }
 
@@ -106,6 +108,9 @@ struct M2LShape {
   static constexpr int NBUF = 1;  // single stage: keeps 3 CTAs/SM with the shared accumulator
   static constexpr int SA = 2 * TT;         // smem accumulator row stride (xor-swizzled columns)
   static constexpr size_t SMEM = (size_t)(NBUF * STAGE + NPAD * SA) * sizeof(double);
+  // unroll of the k-step-pair loops: deeper for small tiles (more loads in
+  // flight), 1 for n_pad >= 224 where registers limit 2 CTAs/SM (measured)
+  static constexpr int KU = FDH_KUNROLL > 0 ? FDH_KUNROLL : (NPAD <= 128 ? 4 : 1);
 };
 
 // stage the moments of the first ncol compacted columns (cnt valid, rest zero)
@@ -132,32 +137,50 @@ template <int NPAD, int NK, int TT, int NTA>
 __device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, NK, TT>::NT][2], const double* __restrict__ Wk,
                                         const double* Bs, int re_off, int im_off, unsigned long long sgn) {
   using S = M2LShape<NPAD, NK, TT>;
+  // W rows are stored k-interleaved in blocks of 8 (k_coupling): the lane's
+  // A-fragment values of k-steps 2p and 2p+1 are adjacent -> one 16-byte load.
   // K half 1: columns of Re A against (Re v, Im v)
-#pragma unroll kKUnroll
-  for (int ks = 0; ks < NK / 4; ++ks) {
-    double a[4], b[NTA];
+#pragma unroll S::KU
+  for (int kp = 0; kp < NK / 8; ++kp) {
+    double2 a[4];
+    double b0[NTA], b1[NTA];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + mt * 8 * S::K2 + 4 * ks);
+    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(reinterpret_cast<const double2*>(Wk + mt * 8 * S::K2 + 8 * kp));
 #pragma unroll
-    for (int nt = 0; nt < NTA; ++nt) b[nt] = Bs[nt * 4 * S::MS + re_off + 4 * ks];
+    for (int nt = 0; nt < NTA; ++nt) {
+      b0[nt] = Bs[nt * 4 * S::MS + re_off + 8 * kp];
+      b1[nt] = Bs[nt * 4 * S::MS + re_off + 8 * kp + 4];
+    }
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].x, b0[nt]);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].y, b1[nt]);
   }
   // K half 2: columns of Im A against (-Im v, Re v)
-#pragma unroll kKUnroll
-  for (int ks = 0; ks < NK / 4; ++ks) {
-    double a[4], b[NTA];
+#pragma unroll S::KU
+  for (int kp = 0; kp < NK / 8; ++kp) {
+    double2 a[4];
+    double b0[NTA], b1[NTA];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(Wk + NK + mt * 8 * S::K2 + 4 * ks);
+    for (int mt = 0; mt < 4; ++mt)
+      a[mt] = __ldg(reinterpret_cast<const double2*>(Wk + NK + mt * 8 * S::K2 + 8 * kp));
 #pragma unroll
-    for (int nt = 0; nt < NTA; ++nt)
-      b[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 4 * ks]) ^ sgn);
+    for (int nt = 0; nt < NTA; ++nt) {
+      b0[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 8 * kp]) ^ sgn);
+      b1[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 8 * kp + 4]) ^ sgn);
+    }
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt], b[nt]);
+      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].x, b0[nt]);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].y, b1[nt]);
   }
 }
 
@@ -266,7 +289,7 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
     if (kk > k0 && !tile_same[kk]) m2l_flush<NPAD, NK, TT>(acc, sacc, tile_cols + (kk - 1) * TT, tile_cnt[kk - 1], warp,
                                                        lane);
     const double* __restrict__ Wk =
-        W + ((int64_t)tile_keys[kk] - key_base) * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + bk;
+        W + ((int64_t)tile_keys[kk] - key_base) * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + 2 * bk;
     const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
     switch ((cnt + 3) >> 2) {  // warp-uniform: only the n-tiles holding columns
       case 1: m2l_key<NPAD, NK, TT, 1>(acc, Wk, Bs, re_off, im_off, sgn); break;
