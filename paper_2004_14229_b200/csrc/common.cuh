@@ -91,3 +91,45 @@ __device__ __forceinline__ void sincos_fast(double x, double* s, double* c) {
   *c = ((q + 1) & 2) ? -cc : cc;
 }
 }  // namespace fdhelm
+
+namespace fdhelm {
+// Coefficients of sincos_fast in the constant bank: FP64 instructions take
+// c[][] operands directly, so the hot loop needs no per-iteration constant
+// materialisation (UMOV pairs) -- see k_p2p.
+__constant__ double c_trig[18] = {
+    6.36619772367581382433e-01,   // 2/pi
+    1.57079632673412561417e+00,   // pio2_1
+    6.07710050630396597660e-11,   // pio2_2
+    2.02226624879595063154e-21,   // pio2_2t
+    1.58969099521155010221e-10,  -2.50507602534068634195e-08, 2.75573137070700676789e-06,
+    -1.98412698298579493134e-04, 8.33333333332248946124e-03,  -1.66666666666666324348e-01,  // sin
+    -1.13596475577881948265e-11, 2.08757232129817482790e-09,  -2.75573143513906633035e-07,
+    2.48015872894767294178e-05,  -1.38888888888741095749e-03, 4.16666666666666019037e-02,   // cos
+    0.5, 1.0};
+
+// sincos_fast without the large-argument guard: the caller guarantees |x| < 1.6e6
+__device__ __forceinline__ void sincos_fast_nc(double x, double* s, double* c) {
+  const double k = rint(x * c_trig[0]);
+  double y = fma(-k, c_trig[1], x);
+  y = fma(-k, c_trig[2], y);
+  y = fma(-k, c_trig[3], y);
+  const double z = y * y;
+  double ps = fma(z, c_trig[4], c_trig[5]);
+  ps = fma(z, ps, c_trig[6]);
+  ps = fma(z, ps, c_trig[7]);
+  ps = fma(z, ps, c_trig[8]);
+  ps = fma(z, ps, c_trig[9]);
+  const double sy = fma(y * z, ps, y);
+  double pc = fma(z, c_trig[10], c_trig[11]);
+  pc = fma(z, pc, c_trig[12]);
+  pc = fma(z, pc, c_trig[13]);
+  pc = fma(z, pc, c_trig[14]);
+  pc = fma(z, pc, c_trig[15]);
+  const double cy = fma(z * z, pc, fma(-c_trig[16], z, c_trig[17]));
+  const int q = (int)(long long)k & 3;
+  const double ss = (q & 1) ? cy : sy;
+  const double cc = (q & 1) ? sy : cy;
+  *s = (q & 2) ? -ss : ss;
+  *c = ((q + 1) & 2) ? -cc : cc;
+}
+}  // namespace fdhelm
