@@ -179,6 +179,7 @@ def run_ours(args, c, rank, world, local_rank):
     x = torch.from_numpy(q.view(np.float64)).to(dev)
     y = torch.empty(2 * c.nt, dtype=torch.float64, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    torch.cuda.synchronize()  # x / y are produced on torch's stream, consumed on the operator's
 
     def step():
         op.apply_device(x.data_ptr(), y.data_ptr(), op.stream())
