@@ -142,6 +142,10 @@ int64_t fdh_export_dirsets(const fdh_op* op, int which, int64_t* rows /*6 cols*/
 /* target leaves owned by this operator (all, or this rank's shard):
  * level, i, j, k, begin, end                                        (6 cols) */
 int64_t fdh_export_owned_leaves(const fdh_op* op, int64_t* rows);
+/* order-independent 64-bit digests of the canonical exports (sum over rows of a
+ * splitmix64 row hash): [T tree+perm, S tree+perm, L+, L-, D/D^ of T, D/D^ of S];
+ * compares structures too large to export (config 4). */
+int fdh_structure_digest(const fdh_op* op, uint64_t* out6);
 
 void fdh_destroy(fdh_op* op);
 const char* fdh_last_error(void);

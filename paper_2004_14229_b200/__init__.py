@@ -28,7 +28,7 @@ ERR_ARG, ERR_DOMAIN, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_MEMORY = 1, 2, 3, 4
 PHASES = ["h2d", "s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "d2h"]
 SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_plan_only", "fdh_apply", "fdh_apply_device", "fdh_stream",
            "fdh_set_timing", "fdh_get_stats", "fdh_export_tree", "fdh_export_perm", "fdh_export_lplus",
-           "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_destroy", "fdh_last_error", "fdh_version",
+           "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_structure_digest", "fdh_destroy", "fdh_last_error", "fdh_version",
            "fdh_fp64_peak_tflops"]
 
 
@@ -89,6 +89,7 @@ def lib():
         L.fdh_destroy.argtypes = [C.c_void_p]
         L.fdh_last_error.restype = C.c_char_p
         L.fdh_version.restype = C.c_char_p
+        L.fdh_structure_digest.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.fdh_fp64_peak_tflops.argtypes = [C.c_int]
         L.fdh_fp64_peak_tflops.restype = C.c_double
         _lib = L
@@ -199,6 +200,11 @@ class DirectionalOperator:
 
     def owned_leaves(self):
         return self._export(lib().fdh_export_owned_leaves, 6)
+
+    def structure_digest(self):
+        out = (C.c_uint64 * 6)()
+        _chk(lib().fdh_structure_digest(self.h, out))
+        return list(out)
 
 
 def version() -> str:

@@ -611,4 +611,10 @@ int64_t fdh_export_dirsets(const fdh_op* o, int which, int64_t* rows) {
 
 int64_t fdh_export_owned_leaves(const fdh_op* o, int64_t* rows) { return o ? export_owned_leaves(o->P, rows) : -1; }
 
+int fdh_structure_digest(const fdh_op* o, uint64_t* out6) {
+  if (!o || !out6) return fail(FDH_ERR_ARG, "NULL argument");
+  structure_digest(o->P, out6);
+  return FDH_OK;
+}
+
 }  // extern "C"

@@ -943,6 +943,77 @@ int64_t export_lminus(const Plan& P, int64_t* rows) {
   std::memcpy(rows, r.data(), sizeof(int64_t) * 8 * n);
   return n;
 }
+// Order-independent 64-bit digests of the canonical exports (sum of splitmix64
+// of each row), for configurations whose lists are too large to export
+// (config 4: 3.47e9 admissible blocks).  out: T tree, S tree, L+, L-, D/D^ (T), D/D^ (S).
+namespace {
+inline uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+inline uint64_t row_hash(const int64_t* v, int n) {
+  uint64_t h = 0x12345678ull;
+  for (int i = 0; i < n; ++i) h = mix64(h ^ (uint64_t)v[i]);
+  return h;
+}
+}  // namespace
+
+void structure_digest(const Plan& P, uint64_t out[6]) {
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  for (int w = 0; w < 2; ++w) {
+    const TreePlan& T = w == 0 ? P.T : P.S;
+    uint64_t acc = 0;
+    for (int l = 0; l <= T.depth; ++l) {
+      const LevelNodes& L = T.lv[l];
+      for (size_t i = 0; i < L.size(); ++i) {
+        const int64_t r[7] = {l, L.ci[i], L.cj[i], L.ck[i], L.begin[i], L.end[i], L.leaf[i]};
+        acc += row_hash(r, 7);
+      }
+    }
+    for (size_t sl = 0; sl < T.perm.size(); ++sl) {
+      const int64_t r[2] = {(int64_t)sl, (int64_t)T.perm[sl]};
+      acc += row_hash(r, 2);
+    }
+    out[w] = acc;
+    uint64_t dacc = 0;
+    for (int l = 0; l <= T.depth; ++l) {
+      const int nd = T.ndir[l];
+      const LevelNodes& L = T.lv[l];
+      for (size_t i = 0; i < L.size(); ++i)
+        for (int c = 0; c < nd; ++c) {
+          const uint8_t k = T.kind[l][i * nd + c];
+          if (!k) continue;
+          const int64_t r[6] = {l, L.ci[i], L.cj[i], L.ck[i], c, k};
+          dacc += row_hash(r, 6);
+        }
+    }
+    out[4 + w] = dacc;
+  }
+  uint64_t lp = 0, lm = 0;
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const LevelNodes& LT = P.T.lv[l];
+    const LevelNodes& LS = P.S.lv[l];
+    uint64_t a = 0;
+#pragma omp parallel for reduction(+ : a)
+    for (int64_t b = 0; b < (int64_t)B.lp_t.size(); ++b) {
+      const int64_t r[8] = {l, LT.ci[B.lp_t[b]], LT.cj[B.lp_t[b]], LT.ck[B.lp_t[b]], LS.ci[B.lp_s[b]], LS.cj[B.lp_s[b]],
+                            LS.ck[B.lp_s[b]], P.key_dir[B.lp_key[b]]};
+      a += row_hash(r, 8);
+    }
+    lp += a;
+    for (size_t b = 0; b < B.lm_t.size(); ++b) {
+      const int64_t r[8] = {l, LT.ci[B.lm_t[b]], LT.cj[B.lm_t[b]], LT.ck[B.lm_t[b]], l, LS.ci[B.lm_s[b]],
+                            LS.cj[B.lm_s[b]], LS.ck[B.lm_s[b]]};
+      lm += row_hash(r, 8);
+    }
+  }
+  out[2] = lp;
+  out[3] = lm;
+}
+
 int64_t export_owned_leaves(const Plan& P, int64_t* rows) {
   int64_t n = (int64_t)P.l2t_level.size();
   if (!rows) return n;

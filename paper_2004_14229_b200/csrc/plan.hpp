@@ -142,6 +142,7 @@ int64_t export_lplus(const Plan& P, int64_t* rows);
 int64_t export_lminus(const Plan& P, int64_t* rows);
 int64_t export_dirsets(const Plan& P, int which, int64_t* rows);
 int64_t export_owned_leaves(const Plan& P, int64_t* rows);
+void structure_digest(const Plan& P, uint64_t out[6]);
 
 // direction conventions
 int num_dirs(int level, int lhf);
