@@ -24,7 +24,7 @@ void launch_l2t(cudaStream_t st, const Consts* C, const double* dirtab, int n_en
                 const int32_t* slot0, const int32_t* nslot, const int64_t* ci, const int64_t* cj,
                 const int64_t* ck, const uint32_t* beg, const uint32_t* end, const double* px,
                 const double* py, const double* pz, const int32_t* slot_dir, const double* loc,
-                double2* y_slot, int n, int n_pad);
+                const double2* y_near, double2* y_slot, int n, int n_pad);
 void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg, const uint32_t* end,
                 const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
                 const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
