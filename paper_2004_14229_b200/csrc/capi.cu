@@ -342,7 +342,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     ++L;
   }
   rec(o, FDH_PHASE_M2L, st);
-  CK(cudaEventRecord(o->ev_q, st));  // charges + moments ready: the near field may start
+  if (o->overlap_nf) CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(P.T.nslots * 2 * np), st));
   if (o->n_item > 0) {
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
@@ -388,19 +388,19 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     rec(o, FDH_NPHASES + 2, st);
     L += 1;
   }
-  // near field (vi) on the second stream.  Default: after the M2L GEMM (it then
-  // overlaps only L2L/L2T; the GEMM keeps the whole GPU and its roofline is
-  // clean).  overlap_nf: concurrent with the GEMM (its CTAs take the slots the
-  // GEMM leaves free) -- measured 0.75 % faster overall on cfg2, GEMM 5 % slower.
-  if (!o->overlap_nf) CK(cudaEventRecord(o->ev_q, st));
-  CK(cudaStreamWaitEvent(o->st2, o->ev_q, 0));
-  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], o->st2));
-  launch_p2p(o->st2, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
+  // near field (vi).  Default: on the main stream right after the M2L GEMM (the
+  // GEMM keeps the whole GPU, phases are sequential).  overlap_nf: on the second
+  // stream, concurrent with the GEMM (its CTAs take the slots the GEMM leaves
+  // free) -- measured 0.75 % faster overall on cfg2, the GEMM itself 5 % slower.
+  cudaStream_t snf = o->overlap_nf ? o->st2 : st;
+  if (o->overlap_nf) CK(cudaStreamWaitEvent(o->st2, o->ev_q, 0));
+  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
+  launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
              o->tz, o->sx, o->sy, o->sz, o->q, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
              o->kappa * P.T.diam[0] * 2.0);
   L += o->n_leaf > 0;
-  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], o->st2));
-  CK(cudaEventRecord(o->ev_nf, o->st2));
+  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
+  if (o->overlap_nf) CK(cudaEventRecord(o->ev_nf, o->st2));
   rec(o, FDH_PHASE_L2L, st);
   for (int l = 0; l < (int)o->l2l.size(); ++l) {
     const LevelDev& D = o->l2l[l];
@@ -410,7 +410,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   }
   rec(o, FDH_PHASE_L2T, st);
   if (o->world > 1) CK(cudaMemsetAsync(o->yslot, 0, sizeof(double2) * (size_t)o->nt, st));
-  CK(cudaStreamWaitEvent(st, o->ev_nf, 0));
+  if (o->overlap_nf) CK(cudaStreamWaitEvent(st, o->ev_nf, 0));
   rec(o, FDH_NPHASES + 5, st);  // L2T proper starts once the near field is done
   launch_l2t(st, o->dC, o->dirtab, o->n_leaf, o->l2t_level, o->l2t_slot0, o->l2t_nslot, o->l2t_ci, o->l2t_cj,
              o->l2t_ck, o->l2t_beg, o->l2t_end, o->tx, o->ty, o->tz, o->tslot_dir, o->loc, o->ynear, o->yslot, n,
@@ -452,7 +452,8 @@ void collect_times(fdh_op* o) {
       CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 5], o->ring[r][FDH_PHASE_L2T + 1]));
       acc[FDH_PHASE_L2T] += ms;
       CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 3], o->ring[r][FDH_NPHASES + 4]));
-      acc[FDH_PHASE_P2P] += ms - 0.0;  // replaces the (empty) sequential P2P slot
+      acc[FDH_PHASE_P2P] += ms;  // replaces the (empty) P2P slot between L2T and D2H
+      if (!o->overlap_nf) acc[FDH_PHASE_M2L] -= ms;  // sequential: it ran inside the M2L interval
       CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_PHASE_P2P], o->ring[r][FDH_PHASE_P2P + 1]));
       acc[FDH_PHASE_P2P] -= ms;
     }
