@@ -14,6 +14,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <string>
+#include <tuple>
 #include <unordered_map>
 
 namespace fdhelm {
@@ -650,6 +652,43 @@ void build_m2l(Plan& P) {
     P.item_seq[i] = P.tile_nitem[tl]++;
     P.item_k0[i] = items[i][2];
     P.item_k1[i] = items[i][3];
+  }
+  // inside every item, order the keys by column map (then key id): runs of keys
+  // with the same map accumulate in registers without a flush (k_m2l_gemm)
+  {
+    const int64_t ni = (int64_t)P.item_tile.size();
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < ni; ++i) {
+      const int64_t b = P.item_k0[i], e = P.item_k1[i];
+      if (e - b < 2) continue;
+      std::vector<int64_t> ord(e - b);
+      for (int64_t j = b; j < e; ++j) ord[j - b] = j;
+      auto key_of = [&](int64_t j) {
+        return std::make_tuple(P.tile_cnt[j],
+                               std::string((const char*)&P.tile_cols[j * TT], (size_t)P.tile_cnt[j]),
+                               P.tile_keys[j]);
+      };
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return key_of(x) > key_of(y); });
+      std::vector<int32_t> keys(e - b), src((e - b) * TT);
+      std::vector<uint8_t> cols((e - b) * TT), cnt(e - b);
+      for (int64_t q = 0; q < e - b; ++q) {
+        const int64_t j = ord[q];
+        keys[q] = P.tile_keys[j];
+        cnt[q] = P.tile_cnt[j];
+        std::copy(P.tile_src.begin() + j * TT, P.tile_src.begin() + (j + 1) * TT, src.begin() + q * TT);
+        std::copy(P.tile_cols.begin() + j * TT, P.tile_cols.begin() + (j + 1) * TT, cols.begin() + q * TT);
+      }
+      for (int64_t q = 0; q < e - b; ++q) {
+        P.tile_keys[b + q] = keys[q];
+        P.tile_cnt[b + q] = cnt[q];
+        std::copy(src.begin() + q * TT, src.begin() + (q + 1) * TT, P.tile_src.begin() + (b + q) * TT);
+        std::copy(cols.begin() + q * TT, cols.begin() + (q + 1) * TT, P.tile_cols.begin() + (b + q) * TT);
+      }
+      for (int64_t j = b; j < e; ++j)
+        P.tile_same[j] = j > b && P.tile_cnt[j - 1] == P.tile_cnt[j] &&
+                         std::equal(P.tile_cols.begin() + j * TT, P.tile_cols.begin() + j * TT + P.tile_cnt[j],
+                                    P.tile_cols.begin() + (j - 1) * TT);
+    }
   }
   // target slots with no M2L contribution
   for (int64_t t = 0; t < T.nslots; ++t)
