@@ -9,8 +9,11 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -473,45 +476,52 @@ void build_worklists(Plan& P) {
 // (almost) the same key list; a tile = `tile` such slots, the union of their
 // keys, and for every key the source slot of each column (-1 if none).
 void build_m2l(Plan& P) {
+  auto mts = std::chrono::steady_clock::now();
+  const bool mdbg = std::getenv("FDH_DEBUG_SETUP") != nullptr;
+#define MTICK(what)                                                                                    \
+  do {                                                                                                 \
+    const auto now_ = std::chrono::steady_clock::now();                                                \
+    if (mdbg) std::fprintf(stderr, "[m2l]   before %-14s %9.1f ms\n", what,                           \
+                           std::chrono::duration<double, std::milli>(now_ - mts).count());           \
+    mts = now_;                                                                                        \
+  } while (0)
   const TreePlan& T = P.T;
   const TreePlan& S = P.S;
   const int TT = P.prm.tile;
-  // pairs (target slot, key, source slot)
+  // pairs (target slot, key, source slot) grouped by target slot: parallel
+  // counting pass, prefix, parallel scatter with atomic cursors (the order
+  // inside a slot is then fixed by the per-slot sort by key -- keys are unique
+  // within a slot, so the result is deterministic)
   int64_t npairs = 0;
   for (auto& B : P.blocks) npairs += (int64_t)B.lp_t.size();
   P.n_c = npairs;
-  std::vector<int32_t> cnt(T.nslots + 1, 0);
-  std::vector<int32_t> pt(npairs), pk(npairs), ps(npairs);
-  {
-    int64_t o = 0;
-    for (int l = 0; l < (int)P.blocks.size(); ++l) {
-      const LevelBlocks& B = P.blocks[l];
-      const int64_t nb = (int64_t)B.lp_t.size();
+  std::unique_ptr<std::atomic<int64_t>[]> cnt(new std::atomic<int64_t>[T.nslots + 1]);
+  for (int64_t i = 0; i <= T.nslots; ++i) cnt[i].store(0, std::memory_order_relaxed);
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const int64_t nb = (int64_t)B.lp_t.size();
 #pragma omp parallel for
-      for (int64_t b = 0; b < nb; ++b) {
-        const int d = P.key_dir[B.lp_key[b]];
-        pt[o + b] = slot_at(T, l, B.lp_t[b], d);
-        ps[o + b] = slot_at(S, l, B.lp_s[b], d);
-        pk[o + b] = B.lp_key[b];
-      }
-      o += nb;
-    }
+    for (int64_t b = 0; b < nb; ++b)
+      cnt[slot_at(T, l, B.lp_t[b], P.key_dir[B.lp_key[b]]) + 1].fetch_add(1, std::memory_order_relaxed);
   }
-  for (int64_t b = 0; b < npairs; ++b) cnt[pt[b] + 1]++;
   std::vector<int64_t> ptr(T.nslots + 1, 0);
-  for (int64_t i = 0; i < T.nslots; ++i) ptr[i + 1] = ptr[i] + cnt[i + 1];
-  std::vector<int32_t> sk(npairs), ss(npairs);
-  {
-    std::vector<int64_t> cur(ptr.begin(), ptr.end() - 1);
-    for (int64_t b = 0; b < npairs; ++b) {
-      const int64_t d = cur[pt[b]]++;
-      sk[d] = pk[b];
-      ss[d] = ps[b];
+  for (int64_t i = 0; i < T.nslots; ++i) ptr[i + 1] = ptr[i] + cnt[i + 1].load(std::memory_order_relaxed);
+  for (int64_t i = 0; i < T.nslots; ++i) cnt[i].store(ptr[i], std::memory_order_relaxed);
+  std::unique_ptr<int32_t[]> skb(new int32_t[std::max<int64_t>(1, npairs)]), ssb(new int32_t[std::max<int64_t>(1, npairs)]);
+  int32_t* sk = skb.get();
+  int32_t* ss = ssb.get();
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    const int64_t nb = (int64_t)B.lp_t.size();
+#pragma omp parallel for
+    for (int64_t b = 0; b < nb; ++b) {
+      const int d = P.key_dir[B.lp_key[b]];
+      const int64_t pos = cnt[slot_at(T, l, B.lp_t[b], d)].fetch_add(1, std::memory_order_relaxed);
+      sk[pos] = B.lp_key[b];
+      ss[pos] = slot_at(S, l, B.lp_s[b], d);
     }
   }
-  std::vector<int32_t>().swap(pt);
-  std::vector<int32_t>().swap(pk);
-  std::vector<int32_t>().swap(ps);
+  MTICK("counting sort");
 #pragma omp parallel for schedule(dynamic, 64)
   for (int64_t t = 0; t < T.nslots; ++t) {
     const int64_t b = ptr[t], e = ptr[t + 1];
@@ -521,6 +531,7 @@ void build_m2l(Plan& P) {
     std::sort(v.begin(), v.end());
     for (int64_t i = b; i < e; ++i) { sk[i] = v[i - b].first; ss[i] = v[i - b].second; }
   }
+  MTICK("slot sort");
   // group target slots (a shard keeps only the slots of its leaves' ancestor closure)
   std::vector<int32_t> ts;
   for (int64_t t = 0; t < T.nslots; ++t)
@@ -544,6 +555,9 @@ void build_m2l(Plan& P) {
   tile_first.push_back((int64_t)ts.size());
   const int64_t ntile = (int64_t)tile_first.size() - 1;
   // a tile never spans two groups: clip at group boundaries
+  std::vector<int32_t> key_lo(64, 0), key_hi(64, 0);
+  for (int32_t k = (int32_t)P.key_level.size() - 1; k >= 0; --k) key_lo[P.key_level[k]] = k;
+  for (int32_t k = 0; k < (int32_t)P.key_level.size(); ++k) key_hi[P.key_level[k]] = k + 1;
   P.tile_level.assign(ntile, 0);
   P.tile_dir.assign(ntile, 0);
   P.tile_tslot.assign(ntile * TT, -1);
@@ -558,16 +572,20 @@ void build_m2l(Plan& P) {
     e = ee;
     P.tile_level[tl] = T.slot_level[ts[b]];
     P.tile_dir[tl] = T.slot_dir[ts[b]];
-    std::vector<int32_t> u;
+    // union of the slots' sorted key lists: dense marks over the level's key range
+    const int32_t kb = key_lo[P.tile_level[tl]], kr = key_hi[P.tile_level[tl]] - kb;
+    std::vector<uint8_t> mark(kr, 0);
     for (int64_t i = b; i < e; ++i) {
       P.tile_tslot[tl * TT + (i - b)] = ts[i];
-      u.insert(u.end(), sk.begin() + ptr[ts[i]], sk.begin() + ptr[ts[i] + 1]);
+      for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) mark[sk[q] - kb] = 1;
     }
-    std::sort(u.begin(), u.end());
-    u.erase(std::unique(u.begin(), u.end()), u.end());
+    std::vector<int32_t> u;
+    for (int32_t k = 0; k < kr; ++k)
+      if (mark[k]) u.push_back(kb + k);
     tcount[tl] = (int64_t)u.size();
     tkeys[tl] = std::move(u);
   }
+  MTICK("tile groups");
   P.tile_kptr.assign(ntile + 1, 0);
   for (int64_t tl = 0; tl < ntile; ++tl) P.tile_kptr[tl + 1] = P.tile_kptr[tl] + tcount[tl];
   const int64_t tot = P.tile_kptr[ntile];
@@ -578,16 +596,17 @@ void build_m2l(Plan& P) {
     const auto& u = tkeys[tl];
     const int64_t base = P.tile_kptr[tl];
     std::copy(u.begin(), u.end(), P.tile_keys.begin() + base);
+    if (u.empty()) continue;
+    const int32_t kb = u.front();
+    std::vector<int32_t> pos(u.back() - kb + 1, -1);  // key -> position in the union
+    for (size_t q = 0; q < u.size(); ++q) pos[u[q] - kb] = (int32_t)q;
     for (int c = 0; c < TT; ++c) {
       const int32_t t = P.tile_tslot[tl * TT + c];
       if (t < 0) continue;
-      size_t q = 0;
-      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) {
-        while (u[q] != sk[i]) ++q;
-        P.tile_src[(base + (int64_t)q) * TT + c] = ss[i];
-      }
+      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) P.tile_src[(base + pos[sk[i] - kb]) * TT + c] = ss[i];
     }
   }
+  MTICK("tile src");
   // compact the valid columns of every (tile, key) to the front
   P.tile_cols.assign(tot * TT, 0);
   P.tile_cnt.assign(tot, 0);
@@ -618,6 +637,7 @@ void build_m2l(Plan& P) {
     }
   }
   P.m2l_cols_exec = exec;
+  MTICK("compaction");
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
   // flight at any moment all work inside ~one chunk of key ids, so each
   // coupling matrix is read from HBM about once and then served from L2 to
@@ -653,6 +673,7 @@ void build_m2l(Plan& P) {
     P.item_k0[i] = items[i][2];
     P.item_k1[i] = items[i][3];
   }
+  MTICK("items");
   // inside every item, order the keys by column map (then key id): runs of keys
   // with the same map accumulate in registers without a flush (k_m2l_gemm)
   {
@@ -690,9 +711,12 @@ void build_m2l(Plan& P) {
                                     P.tile_cols.begin() + (j - 1) * TT);
     }
   }
+  MTICK("item map sort");
   // target slots with no M2L contribution
   for (int64_t t = 0; t < T.nslots; ++t)
     if (ptr[t + 1] == ptr[t]) P.m2l_zero_slots.push_back((int32_t)t);
+  MTICK("end");
+#undef MTICK
 }
 
 }  // namespace
@@ -890,8 +914,20 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
         }
       }
   }
+  auto tick = [&](const char* what, std::chrono::steady_clock::time_point& ts) {
+    const auto now = std::chrono::steady_clock::now();
+    if (std::getenv("FDH_DEBUG_SETUP"))
+      std::fprintf(stderr, "[setup] %-12s %9.1f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - ts).count());
+    ts = now;
+  };
+  auto ts = std::chrono::steady_clock::now();
+  if (std::getenv("FDH_DEBUG_SETUP"))
+    std::fprintf(stderr, "[setup] structure    %9.1f ms\n", P.structure_ms);
   build_worklists(P);
+  tick("worklists", ts);
   build_m2l(P);
+  tick("m2l tiles", ts);
   // statistics
   for (auto& B : P.blocks) {
     P.n_lminus += (int64_t)B.lm_t.size();
