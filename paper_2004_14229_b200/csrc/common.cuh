@@ -107,9 +107,14 @@ __constant__ double c_trig[18] = {
     2.48015872894767294178e-05,  -1.38888888888741095749e-03, 4.16666666666666019037e-02,   // cos
     0.5, 1.0};
 
-// sincos_fast without the large-argument guard: the caller guarantees |x| < 1.6e6
+// sincos_fast without the large-argument guard: the caller guarantees |x| < 1.6e6.
+// k = rint(x 2/pi) via the 1.5*2^52 shifter (one FMA + one add, the quadrant
+// from the shifter's low mantissa bits: no FRND / F2I), sign flips by integer xor.
 __device__ __forceinline__ void sincos_fast_nc(double x, double* s, double* c) {
-  const double k = rint(x * c_trig[0]);
+  const double shifter = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, c_trig[0], shifter);
+  const double k = t - shifter;
+  const int q = __double2loint(t) & 3;
   double y = fma(-k, c_trig[1], x);
   y = fma(-k, c_trig[2], y);
   y = fma(-k, c_trig[3], y);
@@ -126,10 +131,11 @@ __device__ __forceinline__ void sincos_fast_nc(double x, double* s, double* c) {
   pc = fma(z, pc, c_trig[14]);
   pc = fma(z, pc, c_trig[15]);
   const double cy = fma(z * z, pc, fma(-c_trig[16], z, c_trig[17]));
-  const int q = (int)(long long)k & 3;
   const double ss = (q & 1) ? cy : sy;
   const double cc = (q & 1) ? sy : cy;
-  *s = (q & 2) ? -ss : ss;
-  *c = ((q + 1) & 2) ? -cc : cc;
+  const long long sgs = (long long)(q & 2) << 62;        // sin negative in quadrants 2, 3
+  const long long sgc = (long long)((q + 1) & 2) << 62;  // cos negative in quadrants 1, 2
+  *s = __longlong_as_double(__double_as_longlong(ss) ^ sgs);
+  *c = __longlong_as_double(__double_as_longlong(cc) ^ sgc);
 }
 }  // namespace fdhelm
