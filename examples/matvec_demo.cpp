@@ -28,6 +28,18 @@ int main(int argc, char** argv) {
   p.m = m;
   try {
     fdhelm_b200::DirectionalOperator op(tx, ty, tz, sx, sy, sz, lo, hi, p);
+    // the same operator from AoS points and a box type shaped like the
+    // reference's fdhelm::Point3 / fdhelm::AxisBox (geometry.hpp:13-59)
+    struct P3 { double x, y, z; };
+    struct Box { P3 lower, upper; };
+    std::vector<P3> tp(n), sp(n);
+    for (int64_t i = 0; i < n; ++i) { tp[i] = {tx[i], ty[i], tz[i]}; sp[i] = {sx[i], sy[i], sz[i]}; }
+    fdhelm_b200::DirectionalOperator op_aos(std::span<const P3>(tp), std::span<const P3>(sp),
+                                            Box{{0, 0, 0}, {1, 1, 1}}, p);
+    if (op_aos.lplus() != op.lplus() || op_aos.tree(0) != op.tree(0)) {
+      std::fprintf(stderr, "AoS and SoA operators differ\n");
+      return 3;
+    }
     const auto y = op.apply(x);
     double num = 0, den = 0;
     for (int64_t r = 0; r < 64; ++r) {

@@ -8,6 +8,7 @@
 // the reference's exception types: std::invalid_argument (FDH_ERR_ARG, DIM),
 // std::domain_error (FDH_ERR_DOMAIN, singular kernel), std::runtime_error (CUDA).
 #pragma once
+#include <array>
 #include <complex>
 #include <cstdint>
 #include <span>
@@ -42,8 +43,32 @@ inline void check(int rc) {
   }
 }
 
+namespace detail {
+template <class P>
+std::vector<double> axis(std::span<const P> pts, int a) {
+  std::vector<double> v(pts.size());
+  for (size_t i = 0; i < pts.size(); ++i) v[i] = a == 0 ? pts[i].x : (a == 1 ? pts[i].y : pts[i].z);
+  return v;
+}
+}  // namespace detail
+
 class DirectionalOperator {
  public:
+  // AoS points with members x, y, z -- e.g. std::span<const fdhelm::Point3>
+  // (geometry.hpp:13-20) -- and any box with lower / upper points (AxisBox,
+  // geometry.hpp:46-59): the reference's own types work unchanged.
+  template <class Pt, class Box>
+  DirectionalOperator(std::span<const Pt> targets, std::span<const Pt> sources, const Box& root, const Params& p)
+      : DirectionalOperator(detail::axis(targets, 0), detail::axis(targets, 1), detail::axis(targets, 2),
+                            detail::axis(sources, 0), detail::axis(sources, 1), detail::axis(sources, 2),
+                            std::array<double, 3>{root.lower.x, root.lower.y, root.lower.z}.data(),
+                            std::array<double, 3>{root.upper.x, root.upper.y, root.upper.z}.data(), p) {}
+  DirectionalOperator(const std::vector<double>& tx, const std::vector<double>& ty, const std::vector<double>& tz,
+                      const std::vector<double>& sx, const std::vector<double>& sy, const std::vector<double>& sz,
+                      const double* root_lo, const double* root_hi, const Params& p)
+      : DirectionalOperator(std::span<const double>(tx), std::span<const double>(ty), std::span<const double>(tz),
+                            std::span<const double>(sx), std::span<const double>(sy), std::span<const double>(sz),
+                            root_lo, root_hi, p) {}
   // Points as SoA spans (x, y, z) of targets and sources; one shared root box.
   DirectionalOperator(std::span<const double> tx, std::span<const double> ty, std::span<const double> tz,
                       std::span<const double> sx, std::span<const double> sy, std::span<const double> sz,
@@ -76,7 +101,31 @@ class DirectionalOperator {
   }
   fdh_op* handle() { return op_; }
 
+  // canonical introspection (int64 rows, see fdhelm_c.h): the cluster trees
+  // (level, i, j, k, begin, end, leaf), slot -> original index permutations,
+  // admissible blocks L+ (level, t ijk, s ijk, direction), inadmissible L-,
+  // and the direction sets D / D^ (level, ijk, direction, kind)
+  std::vector<int64_t> tree(int which) const { return rows(fdh_export_tree, which, 7); }
+  std::vector<int64_t> perm(int which) const { return rows(fdh_export_perm, which, 1); }
+  std::vector<int64_t> lplus() const { return rows2(fdh_export_lplus, 8); }
+  std::vector<int64_t> lminus() const { return rows2(fdh_export_lminus, 8); }
+  std::vector<int64_t> dirsets(int which) const { return rows(fdh_export_dirsets, which, 6); }
+
  private:
+  template <class F>
+  std::vector<int64_t> rows(F f, int which, int cols) const {
+    const int64_t n = f(op_, which, nullptr);
+    std::vector<int64_t> out((size_t)(n * cols));
+    if (n > 0) f(op_, which, out.data());
+    return out;
+  }
+  template <class F>
+  std::vector<int64_t> rows2(F f, int cols) const {
+    const int64_t n = f(op_, nullptr);
+    std::vector<int64_t> out((size_t)(n * cols));
+    if (n > 0) f(op_, out.data());
+    return out;
+  }
   size_t nt_, ns_;
   fdh_op* op_ = nullptr;
 };

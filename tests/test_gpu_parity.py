@@ -33,7 +33,7 @@ def test_cfg1_full_parity():
     assert np.array_equal(op.apply(q), y)  # bitwise determinism
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("m", [0, 1, 2, 3, 4, 5, 6])
 def test_degrees(m):
     rng = np.random.default_rng(100 + m)
     tg = [rng.random(6000) for _ in range(3)]
