@@ -522,14 +522,23 @@ void build_m2l(Plan& P) {
     }
   }
   MTICK("counting sort");
-#pragma omp parallel for schedule(dynamic, 64)
-  for (int64_t t = 0; t < T.nslots; ++t) {
-    const int64_t b = ptr[t], e = ptr[t + 1];
-    if (e - b < 2) continue;
-    std::vector<std::pair<int32_t, int32_t>> v(e - b);
-    for (int64_t i = b; i < e; ++i) v[i - b] = {sk[i], ss[i]};
-    std::sort(v.begin(), v.end());
-    for (int64_t i = b; i < e; ++i) { sk[i] = v[i - b].first; ss[i] = v[i - b].second; }
+  // per-slot sort by key: keys are ids inside one level, unique within a slot ->
+  // an order-preserving 64-bit pack (key << 32 | source) sorts both at once
+#pragma omp parallel
+  {
+    std::vector<uint64_t> v;
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t t = 0; t < T.nslots; ++t) {
+      const int64_t b = ptr[t], e = ptr[t + 1];
+      if (e - b < 2) continue;
+      v.resize(e - b);
+      for (int64_t i = b; i < e; ++i) v[i - b] = ((uint64_t)(uint32_t)sk[i] << 32) | (uint32_t)ss[i];
+      std::sort(v.begin(), v.end());
+      for (int64_t i = b; i < e; ++i) {
+        sk[i] = (int32_t)(v[i - b] >> 32);
+        ss[i] = (int32_t)(uint32_t)v[i - b];
+      }
+    }
   }
   MTICK("slot sort");
   // group target slots (a shard keeps only the slots of its leaves' ancestor closure)
@@ -574,12 +583,18 @@ void build_m2l(Plan& P) {
     P.tile_dir[tl] = T.slot_dir[ts[b]];
     // union of the slots' sorted key lists: dense marks over the level's key range
     const int32_t kb = key_lo[P.tile_level[tl]], kr = key_hi[P.tile_level[tl]] - kb;
-    std::vector<uint8_t> mark(kr, 0);
+    thread_local std::vector<uint8_t> mark;
+    mark.assign(kr, 0);
+    int64_t nk = 0;
     for (int64_t i = b; i < e; ++i) {
       P.tile_tslot[tl * TT + (i - b)] = ts[i];
-      for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) mark[sk[q] - kb] = 1;
+      for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) {
+        nk += !mark[sk[q] - kb];
+        mark[sk[q] - kb] = 1;
+      }
     }
     std::vector<int32_t> u;
+    u.reserve(nk);
     for (int32_t k = 0; k < kr; ++k)
       if (mark[k]) u.push_back(kb + k);
     tcount[tl] = (int64_t)u.size();
@@ -637,6 +652,13 @@ void build_m2l(Plan& P) {
     }
   }
   P.m2l_cols_exec = exec;
+  if (mdbg) {
+    int64_t hist[17] = {0};
+    for (int64_t i = 0; i < tot; ++i) hist[P.tile_cnt[i]]++;
+    std::fprintf(stderr, "[m2l] tiles %lld  tile-keys %lld  cnt histogram:", (long long)ntile, (long long)tot);
+    for (int c = 1; c <= 16; ++c) std::fprintf(stderr, " %d:%.3f", c, (double)hist[c] / (double)std::max<int64_t>(1, tot));
+    std::fprintf(stderr, "\n");
+  }
   MTICK("compaction");
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
   // flight at any moment all work inside ~one chunk of key ids, so each
