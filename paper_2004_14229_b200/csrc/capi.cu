@@ -80,7 +80,7 @@ struct fdh_op {
   };
   std::vector<Seg> segs;
   int64_t w_slot_keys = 0;
-  double2 *q = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
+  double2 *q = nullptr, *q4 = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
   int* flag = nullptr;
   bool timing = false;
   static constexpr int kRing = 64;
@@ -275,6 +275,7 @@ void setup_device(fdh_op* o) {
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
   o->ticket = o->alloc<int>((size_t)std::max(o->n_tile, 1));
   o->q = o->alloc<double2>((size_t)o->ns);
+  o->q4 = o->alloc<double2>((size_t)o->ns);
   o->yslot = o->alloc<double2>((size_t)o->nt);
   o->ynear = o->alloc<double2>((size_t)o->nt);
   o->xin = o->alloc<double2>((size_t)o->ns);
@@ -328,7 +329,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   CK(cudaEventRecord(o->ev_all[0], st));
   rec(o, FDH_PHASE_H2D, st);
   CK(cudaMemsetAsync(o->flag, 0, sizeof(int), st));
-  launch_gather_charges(st, o->ns, o->perm_s, x, o->q);
+  launch_gather_charges(st, o->ns, o->perm_s, x, o->q, o->q4);
   ++L;
   rec(o, FDH_PHASE_S2M, st);
   launch_s2m(st, o->dC, o->dirtab, o->n_s2m, o->s2m_slot, o->s2m_level, o->s2m_dir, o->s2m_ci, o->s2m_cj, o->s2m_ck,
@@ -396,8 +397,8 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   if (o->overlap_nf) CK(cudaStreamWaitEvent(o->st2, o->ev_q, 0));
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
   launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
-             o->tz, o->sx, o->sy, o->sz, o->q, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
-             o->kappa * P.T.diam[0] * 2.0);
+             o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
+             o->kappa * P.nf_max_dist);
   L += o->n_leaf > 0;
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
   if (o->overlap_nf) CK(cudaEventRecord(o->ev_nf, o->st2));

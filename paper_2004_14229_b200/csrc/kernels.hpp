@@ -8,7 +8,8 @@
 namespace fdhelm {
 
 // ---- k_apply.cu
-void launch_gather_charges(cudaStream_t st, int64_t ns, const uint32_t* perm, const double2* x, double2* q);
+void launch_gather_charges(cudaStream_t st, int64_t ns, const uint32_t* perm, const double2* x, double2* q,
+                           double2* q4);
 void launch_scatter_y(cudaStream_t st, int64_t nt, const uint32_t* perm, const double2* y_slot, double2* y);
 void launch_s2m(cudaStream_t st, const Consts* C, const double* dirtab, int n_entry, const int32_t* slot,
                 const int32_t* level, const int32_t* dir, const int64_t* ci, const int64_t* cj, const int64_t* ck,
@@ -28,7 +29,7 @@ void launch_l2t(cudaStream_t st, const Consts* C, const double* dirtab, int n_en
 void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg, const uint32_t* end,
                 const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
                 const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
-                const double2* q, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
+                const double2* q4, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
                 double2* y_slot, int* flag, double max_phase);
 
 // ---- k_m2l.cu

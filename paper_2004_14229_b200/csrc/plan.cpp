@@ -956,9 +956,22 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
   }
   for (int l = 0; l < (int)P.blocks.size(); ++l) {
     const LevelBlocks& B = P.blocks[l];
-    for (size_t b = 0; b < B.lm_t.size(); ++b)
+    int64_t ext[3] = {0, 0, 0};  // max |lattice offset| per axis over the L- blocks of the level
+    for (size_t b = 0; b < B.lm_t.size(); ++b) {
       P.m_d += (int64_t)(P.T.lv[l].end[B.lm_t[b]] - P.T.lv[l].begin[B.lm_t[b]]) *
                (int64_t)(P.S.lv[l].end[B.lm_s[b]] - P.S.lv[l].begin[B.lm_s[b]]);
+      ext[0] = std::max(ext[0], (int64_t)std::llabs((long long)(P.T.lv[l].ci[B.lm_t[b]] - P.S.lv[l].ci[B.lm_s[b]])));
+      ext[1] = std::max(ext[1], (int64_t)std::llabs((long long)(P.T.lv[l].cj[B.lm_t[b]] - P.S.lv[l].cj[B.lm_s[b]])));
+      ext[2] = std::max(ext[2], (int64_t)std::llabs((long long)(P.T.lv[l].ck[B.lm_t[b]] - P.S.lv[l].ck[B.lm_s[b]])));
+    }
+    if (!B.lm_t.empty()) {  // points of boxes at lattice offset d are at most (|d|+1) sides apart per axis
+      double d2 = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        const double w = (double)(ext[a] + 1) * P.T.side[l][a];
+        d2 += w * w;
+      }
+      P.nf_max_dist = std::max(P.nf_max_dist, 1.0001 * std::sqrt(d2));
+    }
   }
   for (int w = 0; w < 2; ++w) {
     const TreePlan& X = w == 0 ? P.T : P.S;

@@ -123,6 +123,7 @@ struct Plan {
   std::vector<uint8_t> t_leaf_owned;
   std::vector<std::vector<uint8_t>> t_needed;  // [level][node]: owned leaf or ancestor of one
   double shard_cost = 0.0, total_cost = 0.0;     // estimated flops of this shard / of all targets
+  double nf_max_dist = 0.0;  // upper bound of |x_j - y_k| over the near-field pairs
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
