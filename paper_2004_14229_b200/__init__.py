@@ -21,7 +21,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfdhelm_b200.so")
+LIB_PATH = os.environ.get("FDHELM_LIB") or os.path.join(HERE, "libfdhelm_b200.so")  # override: A/B builds
 LHF_DEFAULT = -2
 
 ERR_ARG, ERR_DOMAIN, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_MEMORY = 1, 2, 3, 4, 5, 6

@@ -10,7 +10,13 @@
 //     W = [Re A | Im A],  B(:,2j) = [Re v_j ; -Im v_j],  B(:,2j+1) = [Im v_j ; Re v_j]
 //
 // so that C(:,2j) = Re(A v_j) and C(:,2j+1) = Im(A v_j): the complex product is a
-// single real GEMM with 8 n^2 flops per block.  It runs on
+// single real GEMM with 8 n^2 flops per block.  Groups of 8
+// targets instead use the 3-multiplication (Gauss) product, 6 n^2 flops:
+//     P1 = Re A Re v,  P2 = Im A Im v,  P3 = (Re A + Im A)(Re v + Im v),
+//     Re(A v) = P1 - P2,  Im(A v) = P3 - P1 - P2,
+// with Re A + Im A stored as a third plane of W.  The FP64 tensor pipe and the
+// DFMA pipe share one ~37 TF/s budget on B200 (tools/fp64_mix.cu), so fewer
+// issued flops is the only way past it.  It runs on
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), the only FP64 tensor-core path on
 // sm_100a (tcgen05 has no f64 kind).  Each warp owns 32 rows x 2T columns in
 // registers; A fragments stream from L2 straight into registers (no reuse
@@ -23,6 +29,12 @@
 #ifndef FDH_KUNROLL
 #define FDH_KUNROLL 0
 #endif
+#ifndef FDH_M2L_NBUF
+#define FDH_M2L_NBUF 1
+#endif
+#ifndef FDH_M2L_MINB
+#define FDH_M2L_MINB 0
+#endif
 
 namespace fdhelm {
 
@@ -31,7 +43,8 @@ namespace {
 constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // geometry.hpp:11
 
 // ---------------------------------------------------------- coupling gen
-// W[key][j][k] = Re f_c(xi_t,j, xi_s,k),  W[key][j][n_k + k] = Im f_c(...)
+// W[key][j][k] = Re f_c(xi_t,j, xi_s,k),  W[key][j][n_k + k] = Im f_c(...),
+// W[key][j][2 n_k + k] = Re f_c + Im f_c (the Gauss plane)
 // canonical frame: s at the lattice origin, t at offset d.
 constexpr int kCplRows = 8;
 __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, const double* __restrict__ dirtab,
@@ -54,7 +67,7 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
   const double cv[3] = {c[0], c[1], c[2]};
   const double kappa = C->kappa;
   __syncthreads();
-  double* Wk = W + (key - wbase) * n_pad * 2 * n_k;
+  double* Wk = W + (key - wbase) * n_pad * 3 * n_k;
   for (int idx = threadIdx.x; idx < kCplRows * n_k; idx += blockDim.x) {
     const int j = r0 + idx / n_k, k = idx % n_k;
     if (j >= n_pad) continue;
@@ -74,8 +87,9 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
     // k-interleaved within blocks of 8 (k = 8b + 4h + q stored at 8b + 2q + h), so
     // that a lane's A fragments of two consecutive k-steps are one 16-byte load
     const int kp = (k & ~7) | ((k & 3) << 1) | ((k >> 2) & 1);
-    Wk[(int64_t)j * 2 * n_k + kp] = re;
-    Wk[(int64_t)j * 2 * n_k + n_k + kp] = im;
+    Wk[(int64_t)j * 3 * n_k + kp] = re;
+    Wk[(int64_t)j * 3 * n_k + n_k + kp] = im;
+    Wk[(int64_t)j * 3 * n_k + 2 * n_k + kp] = re + im;  // Gauss plane
   }
 }
 
@@ -97,20 +111,55 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int NPAD, int NK, int TT>
 struct M2LShape {
-  static constexpr int K2 = 2 * NK;         // GEMM K (and W row length)
+  static constexpr int K3 = 3 * NK;         // W row length: [Re A | Im A | Re A + Im A]
   static constexpr int GS = 2 * NPAD;       // moment slot stride in HBM ([Re | Im] planes of NPAD)
-  static constexpr int MS = 2 * NK + 8 + ((NK & 8) ? 0 : 0);  // smem moment stride (== 8 mod 16)
-  static constexpr int IMOFF = NK + 4;      // smem offset of the imaginary plane (== 4 or 12 mod 16)
-  static_assert(NK % 8 == 0 && MS % 16 == 8, "bank-conflict-free B fragments");
-  static constexpr int NT = 2 * TT / 8;     // 8-column n-tiles per warp
-  static constexpr int THREADS = NPAD;      // one warp per 32 rows
+  // smem moment column: [Re (NK) | pad | Im (NK) | pad], IMOFF == 8 and MS == 4 (mod 16):
+  // both B-fragment patterns (4 columns x Re/Im x 4 k, and 4 columns x 4 k per
+  // half-warp) hit 16 distinct 8-byte banks
+  static constexpr int IMOFF = NK + ((NK % 16 == 0) ? 8 : 0);
+  static constexpr int MS = IMOFF + NK + ((4 - (IMOFF + NK)) % 16 + 16) % 16;
+  static_assert(NK % 8 == 0 && IMOFF % 16 == 8 && MS % 16 == 4, "bank-conflict-free B fragments");
+  // Gauss product for n_pad <= 128; above, its 1.5x accumulators would cost a
+  // resident CTA (n_pad 224: 2 -> 1 CTA/SM), so the real GEMM keeps all 4 n-tiles
+  static constexpr bool GAUSS = m2l_gauss(NPAD);
+  static_assert(GAUSS || TT == 16, "32-target tiles use the Gauss scheme");
+  // rows per warp: 32 (4 m-tiles) for 16-target tiles; 16 (2 m-tiles) for 32-target
+  // tiles, which keeps the accumulators at 48 doubles and halves the W (A operand)
+  // bytes per DMMA -- the L2 -> SM stream of W is what bounds the GEMM
+  static constexpr int RW = TT == 32 ? 16 : 32;
+  static constexpr int MT = RW / 8;
+  static constexpr int THREADS = NPAD / RW * 32;
   static constexpr int STAGE = TT * MS;     // doubles per smem stage
-  static constexpr int NBUF = 1;  // single stage: keeps 3 CTAs/SM with the shared accumulator
+  // moment stages: 2 overlaps the staging of key k+1 with the DMMAs of key k.
+  // 16-target tiles: measured 10 % slower on config 2 (55 -> 61 ms, 2 CTAs/SM),
+  // so 1; 32-target tiles run 1 CTA/SM and need the overlap
+  static constexpr int NBUF = TT == 32 ? 2 : FDH_M2L_NBUF;
   static constexpr int SA = 2 * TT;         // smem accumulator row stride (xor-swizzled columns)
-  static constexpr size_t SMEM = (size_t)(NBUF * STAGE + NPAD * SA) * sizeof(double);
-  // unroll of the k-step-pair loops: deeper for small tiles (more loads in
-  // flight), 1 for n_pad >= 224 where registers limit 2 CTAs/SM (measured)
-  static constexpr int KU = FDH_KUNROLL > 0 ? FDH_KUNROLL : (NPAD <= 128 ? 4 : 1);
+  // per-key metadata of the item (key id, cnt, same flag, TT source slots and
+  // TT target columns) staged in smem windows of MK keys: the per-key loads
+  // are off the critical path (they miss L2: each item reads its slice once)
+  static constexpr int MK = 64;
+  static constexpr int META = MK * (4 + 1 + 1 + 5 * TT);  // bytes
+  static constexpr size_t SMEM = (size_t)(NBUF * STAGE + NPAD * SA) * sizeof(double) + (META + 15) / 16 * 16;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  // unroll of the k-step-pair loops
+  static constexpr int KU = FDH_KUNROLL > 0 ? FDH_KUNROLL : (NPAD <= 128 ? 2 : 1);
+  // resident CTAs per SM the register allocation must allow
+  static constexpr int MINB = FDH_M2L_MINB > 0 ? FDH_M2L_MINB : (NPAD == 224 ? 2 : 1);
+  static constexpr int NG = GAUSS ? TT / 8 : 1;  // Gauss n-tiles held (1 = unused)
+  static constexpr int NO = GAUSS ? 1 : TT / 4;  // real-GEMM n-tiles held
+  // A fragments prefetched one k-step pair ahead in registers (Gauss shapes;
+  // the n_pad >= 224 shapes have no registers to spare at 2 CTAs/SM)
+  static constexpr bool PF = GAUSS;
+};
+
+// register accumulators of one warp (RW rows = MT m-tiles):
+//   g[p][mt][nt][2]: Gauss products p = P1, P2, P3 of the 8-target n-tiles nt < NG
+//   o[mt][nt][2]:    (Re, Im) of the 4-target n-tiles nt < NO of the real GEMM
+template <int MT, int NG, int NO>
+struct M2LAcc {
+  double g[3][MT][NG][2];
+  double o[MT][NO][2];
 };
 
 // stage the moments of the first ncol compacted columns (cnt valid, rest zero)
@@ -131,78 +180,167 @@ __device__ __forceinline__ void m2l_stage(double* buf, const int32_t* __restrict
     }
   }
 }
+__device__ __forceinline__ int m2l_ncol(M2LSplit sp) { return 8 * sp.a3 + 4 * sp.ao; }
 
-// One key: C[:, n-tiles < NTA] += W_key * B over K = 2 NPAD.
-template <int NPAD, int NK, int TT, int NTA>
-__device__ __forceinline__ void m2l_key(double (&acc)[4][M2LShape<NPAD, NK, TT>::NT][2], const double* __restrict__ Wk,
-                                        const double* Bs, int re_off, int im_off, unsigned long long sgn) {
+// A fragments of one k-step pair: MT m-tiles x (k-step 2kp, 2kp+1), 16-byte loads
+template <int K3, int MT>
+__device__ __forceinline__ void m2l_lda(double2 (&a)[MT], const double* __restrict__ p) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) a[mt] = __ldg(reinterpret_cast<const double2*>(p + mt * 8 * K3));
+}
+
+// DMMAs of one k-step pair of plane PL (0: Re A, 1: Im A, 2: Re A + Im A)
+template <int NPAD, int NK, int TT, int A3, int AO, int PL, class Acc>
+__device__ __forceinline__ void m2l_step(Acc& acc, const double2 (&a)[M2LShape<NPAD, NK, TT>::MT], const double* Bg,
+                                         const double* Bo, int kp, int re_off, int im_off, unsigned long long sgn) {
   using S = M2LShape<NPAD, NK, TT>;
-  // W rows are stored k-interleaved in blocks of 8 (k_coupling): the lane's
-  // A-fragment values of k-steps 2p and 2p+1 are adjacent -> one 16-byte load.
-  // K half 1: columns of Re A against (Re v, Im v)
-#pragma unroll S::KU
-  for (int kp = 0; kp < NK / 8; ++kp) {
-    double2 a[4];
-    double b0[NTA], b1[NTA];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) a[mt] = __ldg(reinterpret_cast<const double2*>(Wk + mt * 8 * S::K2 + 8 * kp));
+  for (int h = 0; h < 2; ++h) {
+    const int ko = 8 * kp + 4 * h;
+    double bg[A3 > 0 ? A3 : 1], bo[AO > 0 ? AO : 1];
 #pragma unroll
-    for (int nt = 0; nt < NTA; ++nt) {
-      b0[nt] = Bs[nt * 4 * S::MS + re_off + 8 * kp];
-      b1[nt] = Bs[nt * 4 * S::MS + re_off + 8 * kp + 4];
+    for (int nt = 0; nt < A3; ++nt) {
+      const double* q = Bg + nt * 8 * S::MS + ko;
+      bg[nt] = PL == 0 ? q[0] : (PL == 1 ? q[S::IMOFF] : q[0] + q[S::IMOFF]);  // P1: Re v, P2: Im v, P3: sum
     }
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].x, b0[nt]);
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].y, b1[nt]);
-  }
-  // K half 2: columns of Im A against (-Im v, Re v)
-#pragma unroll S::KU
-  for (int kp = 0; kp < NK / 8; ++kp) {
-    double2 a[4];
-    double b0[NTA], b1[NTA];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-      a[mt] = __ldg(reinterpret_cast<const double2*>(Wk + NK + mt * 8 * S::K2 + 8 * kp));
-#pragma unroll
-    for (int nt = 0; nt < NTA; ++nt) {
-      b0[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 8 * kp]) ^ sgn);
-      b1[nt] = __longlong_as_double(__double_as_longlong(Bs[nt * 4 * S::MS + im_off + 8 * kp + 4]) ^ sgn);
+    for (int nt = 0; nt < AO; ++nt) {
+      if (PL == 0) bo[nt] = Bo[nt * 4 * S::MS + re_off + ko];
+      // -Im by an integer xor of the sign bit (keeps the FP64 pipe for DMMA)
+      if (PL == 1) bo[nt] = __longlong_as_double(__double_as_longlong(Bo[nt * 4 * S::MS + im_off + ko]) ^ sgn);
     }
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < S::MT; ++mt) {
+      const double av = h ? a[mt].y : a[mt].x;
 #pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].x, b0[nt]);
+      for (int nt = 0; nt < A3; ++nt) dmma8x8x4(acc.g[PL][mt][nt], av, bg[nt]);
+      if (PL < 2) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NTA; ++nt) dmma8x8x4(acc[mt][nt], a[mt].y, b1[nt]);
+        for (int nt = 0; nt < AO; ++nt) dmma8x8x4(acc.o[mt][nt], av, bo[nt]);
+      }
+    }
   }
+}
+
+// One key.  A3 Gauss n-tiles (targets 0 .. 8 A3-1) and AO real-GEMM n-tiles
+// (targets 8 A3 .. 8 A3 + 4 AO - 1); the A fragments of the Re / Im planes are
+// shared by both schemes.  The A stream is software-pipelined one k-step pair
+// ahead when S::PF (a holds the current pair on entry; the planes are contiguous
+// in a W row, so the next pair is always 8 doubles on), and the last pair
+// prefetches the first pair of the next key (Wn, null at the end of the item).
+//   Wk: lane's W row (k-interleaved, see k_coupling) at k offset 2 bk
+//   Bg: smem + (lane >> 2) * MS + bk          (Gauss: column = target)
+//   Bo: smem + (8 A3 + (lane >> 3)) * MS + bk (real GEMM: column pair per target)
+template <int NPAD, int NK, int TT, int A3, int AO, class Acc>
+__device__ __forceinline__ void m2l_key(Acc& acc, double2 (&a)[M2LShape<NPAD, NK, TT>::MT],
+                                        const double* __restrict__ Wk, const double* __restrict__ Wn, const double* Bg,
+                                        const double* Bo, int re_off, int im_off, unsigned long long sgn) {
+  using S = M2LShape<NPAD, NK, TT>;
+  constexpr int NKP = NK / 8, MT = S::MT;
+  constexpr int NPL = A3 > 0 ? 3 : 2;
+#pragma unroll
+  for (int pl = 0; pl < NPL; ++pl) {
+#pragma unroll S::KU
+    for (int kp = 0; kp < NKP; ++kp) {
+      double2 an[MT];
+      if constexpr (S::PF) {
+        const double* nx = (pl + 1 < NPL || kp + 1 < NKP) ? Wk + 8 * (pl * NKP + kp + 1) : Wn;
+        if (nx) m2l_lda<S::K3, MT>(an, nx);
+      } else {
+        m2l_lda<S::K3, MT>(a, Wk + 8 * (pl * NKP + kp));
+      }
+      if (pl == 0) m2l_step<NPAD, NK, TT, A3, AO, 0>(acc, a, Bg, Bo, kp, re_off, im_off, sgn);
+      else if (pl == 1) m2l_step<NPAD, NK, TT, A3, AO, 1>(acc, a, Bg, Bo, kp, re_off, im_off, sgn);
+      else m2l_step<NPAD, NK, TT, A3, AO, 2>(acc, a, Bg, Bo, kp, re_off, im_off, sgn);
+      if constexpr (S::PF) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
+      }
+    }
+  }
+}
+
+// dispatch on the split of the key (warp-uniform): only the n-tiles holding columns
+template <int NPAD, int NK, int TT, class Acc>
+__device__ __forceinline__ void m2l_key_dispatch(M2LSplit sp, Acc& acc, double2 (&a)[M2LShape<NPAD, NK, TT>::MT],
+                                                 const double* Wk, const double* Wn, const double* Bg,
+                                                 const double* Bo, int re_off, int im_off, unsigned long long sgn) {
+  using S = M2LShape<NPAD, NK, TT>;
+#define FDH_KEY(A3, AO) m2l_key<NPAD, NK, TT, A3, AO>(acc, a, Wk, Wn, Bg, Bo, re_off, im_off, sgn)
+  if constexpr (S::GAUSS) {
+    switch (sp.a3 * 2 + sp.ao) {
+      case 1: FDH_KEY(0, 1); break;
+      case 2: FDH_KEY(1, 0); break;
+      case 3: FDH_KEY(1, 1); break;
+      case 4: FDH_KEY(2, 0); break;
+      default:
+        if constexpr (S::NG >= 4) {
+          switch (sp.a3 * 2 + sp.ao) {
+            case 5: FDH_KEY(2, 1); break;
+            case 6: FDH_KEY(3, 0); break;
+            case 7: FDH_KEY(3, 1); break;
+            default: FDH_KEY(4, 0); break;
+          }
+        }
+        break;
+    }
+  } else {
+    switch (sp.ao) {
+      case 1: FDH_KEY(0, 1); break;
+      case 2: FDH_KEY(0, 2); break;
+      case 3: FDH_KEY(0, 3); break;
+      default: FDH_KEY(0, 4); break;
+    }
+  }
+#undef FDH_KEY
 }
 
 // add the register tile (compacted columns) into the shared accumulator of the
 // tile's target columns; every (row, target) belongs to one lane: no races
-template <int NPAD, int NK, int TT>
-__device__ __forceinline__ void m2l_flush(double (&acc)[4][M2LShape<NPAD, NK, TT>::NT][2], double* sacc,
-                                          const uint8_t* __restrict__ cols, int cnt, int warp, int lane) {
+template <int NPAD, int NK, int TT, class Acc>
+__device__ __forceinline__ void m2l_flush(Acc& acc, double* sacc, const uint8_t* __restrict__ cols, int cnt,
+                                          int warp, int lane) {
   using S = M2LShape<NPAD, NK, TT>;
+  const M2LSplit sp = m2l_split(cnt, S::GAUSS);
+  const int rbase = warp * S::RW + (lane >> 2);
+  // Gauss n-tiles: lane holds targets 8 nt + 2 (lane & 3) + e
 #pragma unroll
-  for (int nt = 0; nt < S::NT; ++nt) {
-    const int j = nt * 4 + (lane & 3);
-    const int t = j < cnt ? cols[j] : -1;
+  for (int nt = 0; nt < S::NG; ++nt) {
+    if (S::GAUSS && nt < sp.a3) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      if (t >= 0) {
-        const int row = warp * 32 + mt * 8 + (lane >> 2);
-        double* p = sacc + row * S::SA + 2 * (t ^ (row & (TT - 1)));
-        p[0] += acc[mt][nt][0];
-        p[1] += acc[mt][nt][1];
+      for (int e = 0; e < 2; ++e) {
+        const int j = nt * 8 + 2 * (lane & 3) + e;
+        const int t = j < cnt ? cols[j] : -1;
+#pragma unroll
+        for (int mt = 0; mt < S::MT; ++mt) {
+          if (t >= 0) {
+            const int row = rbase + mt * 8;
+            const double p1 = acc.g[0][mt][nt][e], p2 = acc.g[1][mt][nt][e], p3 = acc.g[2][mt][nt][e];
+            double* p = sacc + row * S::SA + 2 * (t ^ (row & (TT - 1)));
+            p[0] += p1 - p2;
+            p[1] += p3 - (p1 + p2);
+          }
+          acc.g[0][mt][nt][e] = acc.g[1][mt][nt][e] = acc.g[2][mt][nt][e] = 0.0;
+        }
       }
-      acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    }
+  }
+  // real-GEMM n-tiles: lane holds target 8 a3 + 4 nt + (lane & 3), (Re, Im)
+#pragma unroll
+  for (int nt = 0; nt < S::NO; ++nt) {
+    if (nt < sp.ao) {
+      const int j = sp.a3 * 8 + nt * 4 + (lane & 3);
+      const int t = j < cnt ? cols[j] : -1;
+#pragma unroll
+      for (int mt = 0; mt < S::MT; ++mt) {
+        if (t >= 0) {
+          const int row = rbase + mt * 8;
+          double* p = sacc + row * S::SA + 2 * (t ^ (row & (TT - 1)));
+          p[0] += acc.o[mt][nt][0];
+          p[1] += acc.o[mt][nt][1];
+        }
+        acc.o[mt][nt][0] = acc.o[mt][nt][1] = 0.0;
+      }
     }
   }
 }
@@ -226,7 +364,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // dispatched first, so the wait is short and cannot deadlock); the last item
 // writes the locals.  Summation order is fixed -> bitwise deterministic.
 template <int NPAD, int NK, int TT>
-__global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ item_tile,
+__global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD, NK, TT>::MINB) k_m2l_gemm(const int32_t* __restrict__ item_tile,
                                                    const int32_t* __restrict__ item_seq,
                                                    const int64_t* __restrict__ item_k0,
                                                    const int64_t* __restrict__ item_k1,
@@ -242,20 +380,45 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
                                                    double* __restrict__ loc, int* __restrict__ err, int item0,
                                                    int64_t key_base) {
   using S = M2LShape<NPAD, NK, TT>;
-  constexpr int NT = S::NT;
-  static_assert(NT == 4, "one warp row-block covers 4 n-tiles");
+  constexpr int MT = S::MT;
   extern __shared__ __align__(16) double smem[];
   double* sacc = smem + S::NBUF * S::STAGE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = item0 + (int)blockIdx.x;
   const int64_t k0 = item_k0[item], k1 = item_k1[item];
+  // metadata window [w0, w0 + MK)
+  int32_t* m_src = reinterpret_cast<int32_t*>(sacc + NPAD * S::SA);
+  int32_t* m_key = m_src + S::MK * TT;
+  uint8_t* m_cols = reinterpret_cast<uint8_t*>(m_key + S::MK);
+  uint8_t* m_cnt = m_cols + S::MK * TT;
+  uint8_t* m_same = m_cnt + S::MK;
+  int64_t w0 = k0;
+  auto load_meta = [&](int64_t b) {
+    const int n = (int)min((int64_t)S::MK, k1 - b);
+    for (int i = threadIdx.x; i < n; i += S::THREADS) {
+      m_key[i] = tile_keys[b + i];
+      m_cnt[i] = tile_cnt[b + i];
+      m_same[i] = tile_same[b + i];
+    }
+    for (int i = threadIdx.x; i < n * TT; i += S::THREADS) {
+      m_src[i] = tile_src[b * TT + i];
+      m_cols[i] = tile_cols[b * TT + i];
+    }
+    __syncthreads();
+  };
+  load_meta(k0);
 
   for (int i = threadIdx.x; i < NPAD * S::SA; i += S::THREADS) sacc[i] = 0.0;
-  double acc[4][NT][2];
+  M2LAcc<MT, S::NG, S::NO> acc;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int nt = 0; nt < S::NO; ++nt) acc.o[mt][nt][0] = acc.o[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int nt = 0; nt < S::NG; ++nt) acc.g[p][mt][nt][0] = acc.g[p][mt][nt][1] = 0.0;
+  }
 
   // B fragment addressing: lane holds B[k0 + (lane&3)][nt*8 + lane/4]
   //   column col = nt*8 + lane/4 -> source c = nt*4 + lane/8, parity = (lane>>2)&1
@@ -268,17 +431,28 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
   const unsigned long long sgn = bpar ? 0ull : 0x8000000000000000ull;
 
   {
-    const int c0 = tile_cnt[k0];
-    m2l_stage<NPAD, NK, TT>(smem, tile_src + k0 * TT, c0, 4 * ((c0 + 3) >> 2), mom);
+    const int c0 = m_cnt[0];
+    m2l_stage<NPAD, NK, TT>(smem, m_src, c0, m2l_ncol(m2l_split(c0, S::GAUSS)), mom);
   }
   cp_async_commit();
+  // lane's W row (k-interleaved, offset 2 bk) without the key offset; first A pair of key k0
+  const double* __restrict__ Wrow = W + (int64_t)(warp * S::RW + (lane >> 2)) * S::K3 + 2 * bk;
+  double2 a[MT];
+  if constexpr (S::PF) m2l_lda<S::K3, MT>(a, Wrow + ((int64_t)m_key[0] - key_base) * NPAD * S::K3);
   int stage = 0;
   for (int64_t kk = k0; kk < k1; ++kk) {
-    const int cnt = tile_cnt[kk];
-    if constexpr (S::NBUF == 2) {
+    if (kk + 1 < k1 && kk + 1 - w0 >= S::MK) {  // slide the window to [kk - 1, ...)
+      __syncthreads();
+      w0 = kk - 1;
+      load_meta(w0);
+    }
+    const int j = (int)(kk - w0);
+    const int cnt = m_cnt[j];
+    if constexpr (S::NBUF == 2) {  // stage key kk+1 into the other buffer, wait for key kk
       if (kk + 1 < k1) {
-        const int cn = tile_cnt[kk + 1];
-        m2l_stage<NPAD, NK, TT>(smem + (stage ^ 1) * S::STAGE, tile_src + (kk + 1) * TT, cn, 4 * ((cn + 3) >> 2), mom);
+        const int cn = m_cnt[j + 1];
+        m2l_stage<NPAD, NK, TT>(smem + (stage ^ 1) * S::STAGE, m_src + (j + 1) * TT, cn,
+                                m2l_ncol(m2l_split(cn, S::GAUSS)), mom);
       }
       cp_async_commit();
       cp_async_wait<1>();
@@ -286,29 +460,26 @@ __global__ void __launch_bounds__(NPAD) k_m2l_gemm(const int32_t* __restrict__ i
       cp_async_wait<0>();
     }
     __syncthreads();
-    if (kk > k0 && !tile_same[kk]) m2l_flush<NPAD, NK, TT>(acc, sacc, tile_cols + (kk - 1) * TT, tile_cnt[kk - 1], warp,
-                                                       lane);
-    const double* __restrict__ Wk =
-        W + ((int64_t)tile_keys[kk] - key_base) * NPAD * S::K2 + (int64_t)(warp * 32 + (lane >> 2)) * S::K2 + 2 * bk;
-    const double* Bs = smem + stage * S::STAGE + bcol * S::MS + bk;
-    switch ((cnt + 3) >> 2) {  // warp-uniform: only the n-tiles holding columns
-      case 1: m2l_key<NPAD, NK, TT, 1>(acc, Wk, Bs, re_off, im_off, sgn); break;
-      case 2: m2l_key<NPAD, NK, TT, 2>(acc, Wk, Bs, re_off, im_off, sgn); break;
-      case 3: m2l_key<NPAD, NK, TT, 3>(acc, Wk, Bs, re_off, im_off, sgn); break;
-      default: m2l_key<NPAD, NK, TT, 4>(acc, Wk, Bs, re_off, im_off, sgn); break;
-    }
+    if (kk > k0 && !m_same[j]) m2l_flush<NPAD, NK, TT>(acc, sacc, m_cols + (j - 1) * TT, m_cnt[j - 1], warp, lane);
+    const double* Bst = smem + stage * S::STAGE;
+    const double* Bg = Bst + (lane >> 2) * S::MS + bk;
+    const M2LSplit sp = m2l_split(cnt, S::GAUSS);
+    const double* Bo = Bst + (8 * sp.a3 + bcol) * S::MS + bk;
+    const double* __restrict__ Wk = Wrow + ((int64_t)m_key[j] - key_base) * NPAD * S::K3;
+    const double* __restrict__ Wn = kk + 1 < k1 ? Wrow + ((int64_t)m_key[j + 1] - key_base) * NPAD * S::K3 : nullptr;
+    m2l_key_dispatch<NPAD, NK, TT>(sp, acc, a, Wk, Wn, Bg, Bo, re_off, im_off, sgn);
     __syncthreads();
     if constexpr (S::NBUF == 2) {
       stage ^= 1;
     } else {
       if (kk + 1 < k1) {
-        const int cn = tile_cnt[kk + 1];
-        m2l_stage<NPAD, NK, TT>(smem, tile_src + (kk + 1) * TT, cn, 4 * ((cn + 3) >> 2), mom);
+        const int cn = m_cnt[j + 1];
+        m2l_stage<NPAD, NK, TT>(smem, m_src + (j + 1) * TT, cn, m2l_ncol(m2l_split(cn, S::GAUSS)), mom);
       }
       cp_async_commit();
     }
   }
-  m2l_flush<NPAD, NK, TT>(acc, sacc, tile_cols + (k1 - 1) * TT, tile_cnt[k1 - 1], warp, lane);
+  m2l_flush<NPAD, NK, TT>(acc, sacc, m_cols + (k1 - 1 - w0) * TT, m_cnt[k1 - 1 - w0], warp, lane);
   __syncthreads();
   // ---- chained accumulation into the tile (chunk order)
   const int tile = item_tile[item], seq = item_seq[item], nit = tile_nitem[tile];
@@ -381,6 +552,14 @@ void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int
 
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a) {
   if (a.n_item <= 0) return 0;
+  if (tile == 32) {
+    if (n_pad == 32 && n_k == 8) run_gemm<32, 8, 32>(st, a);
+    else if (n_pad == 32 && n_k == 32) run_gemm<32, 32, 32>(st, a);
+    else if (n_pad == 64 && n_k == 64) run_gemm<64, 64, 32>(st, a);
+    else if (n_pad == 128 && n_k == 128) run_gemm<128, 128, 32>(st, a);
+    else return 1;
+    return 0;
+  }
   if (tile != 16) return 1;
   if (n_pad == 32 && n_k == 8) run_gemm<32, 8, 16>(st, a);
   else if (n_pad == 32 && n_k == 32) run_gemm<32, 32, 16>(st, a);

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "m2l_split.hpp"
 
 namespace fdhelm {
 

@@ -487,6 +487,8 @@ void build_m2l(Plan& P) {
   } while (0)
   const TreePlan& T = P.T;
   const TreePlan& S = P.S;
+  if (const char* e = std::getenv("FDH_M2L_TILE")) P.prm.tile = std::atoi(e) == 32 ? 32 : 16;  // tuning knob
+  if (!m2l_gauss(P.n_pad)) P.prm.tile = 16;  // 32-target tiles exist for the Gauss shapes only
   const int TT = P.prm.tile;
   // pairs (target slot, key, source slot) grouped by target slot: parallel
   // counting pass, prefix, parallel scatter with atomic cursors (the order
@@ -648,15 +650,17 @@ void build_m2l(Plan& P) {
           std::equal(P.tile_cols.begin() + i * TT, P.tile_cols.begin() + i * TT + cnt,
                      P.tile_cols.begin() + (i - 1) * TT))
         P.tile_same[i] = 1;
-      exec += 4 * ((cnt + 3) / 4);
+      const M2LSplit sp = m2l_split(cnt, m2l_gauss(P.n_pad));
+      exec += 3 * sp.a3 + 2 * sp.ao;
     }
   }
-  P.m2l_cols_exec = exec;
+  P.m2l_units_exec = exec;
   if (mdbg) {
-    int64_t hist[17] = {0};
+    int64_t hist[257] = {0};
     for (int64_t i = 0; i < tot; ++i) hist[P.tile_cnt[i]]++;
-    std::fprintf(stderr, "[m2l] tiles %lld  tile-keys %lld  cnt histogram:", (long long)ntile, (long long)tot);
-    for (int c = 1; c <= 16; ++c) std::fprintf(stderr, " %d:%.3f", c, (double)hist[c] / (double)std::max<int64_t>(1, tot));
+    std::fprintf(stderr, "[m2l] tiles %lld  tile-keys %lld  units %lld  cnt histogram:", (long long)ntile,
+                 (long long)tot, (long long)P.m2l_units_exec);
+    for (int c = 1; c <= TT; ++c) std::fprintf(stderr, " %d:%.3f", c, (double)hist[c] / (double)std::max<int64_t>(1, tot));
     std::fprintf(stderr, "\n");
   }
   MTICK("compaction");
@@ -665,7 +669,7 @@ void build_m2l(Plan& P) {
   // coupling matrix is read from HBM about once and then served from L2 to
   // every tile that uses it.  Chunk width: ~12 MB of coupling matrices.  The
   // items of one tile are chained in chunk order (item_seq) by the kernel.
-  const int64_t wbytes = (int64_t)P.n_pad * 2 * P.n_k * 8;
+  const int64_t wbytes = (int64_t)P.n_pad * 3 * P.n_k * 8;
   int64_t chunk_mb = 12;  // measured optimum 8-12 MB on config 2 (profiles/r01_m2l_chunk_sweep.txt)
   if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
   const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
@@ -734,6 +738,13 @@ void build_m2l(Plan& P) {
     }
   }
   MTICK("item map sort");
+  if (mdbg) {
+    int64_t flushes = 0;
+    for (size_t i = 0; i < P.item_k0.size(); ++i)
+      for (int64_t j = P.item_k0[i]; j < P.item_k1[i]; ++j) flushes += (j == P.item_k0[i] || !P.tile_same[j]);
+    std::fprintf(stderr, "[m2l] items %lld  column-map runs %lld (%.2f keys per run)\n", (long long)P.item_k0.size(),
+                 (long long)flushes, (double)tot / (double)std::max<int64_t>(1, flushes));
+  }
   // target slots with no M2L contribution
   for (int64_t t = 0; t < T.nslots; ++t)
     if (ptr[t + 1] == ptr[t]) P.m2l_zero_slots.push_back((int32_t)t);

@@ -13,12 +13,14 @@
 // stable octant partition); canonical (level, i, j, k) order is produced only
 // by the export functions.
 #pragma once
+#include "m2l_split.hpp"
 #include <array>
 #include <cstdint>
 #include <string>
 #include <vector>
 
 namespace fdhelm {
+
 
 struct PlanError {
   int code;
@@ -127,7 +129,7 @@ struct Plan {
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
-  int64_t m2l_cols_exec = 0;  // executed target columns (4 * ceil(cnt / 4) per tile key)
+  int64_t m2l_units_exec = 0;  // issued DMMA work in M2LSplit units (16 n_pad n_k flop each)
   double setup_ms = 0.0;
   double structure_ms = 0.0;  // trees + partition + directions + slots
 };
