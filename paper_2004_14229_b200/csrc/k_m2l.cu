@@ -125,7 +125,8 @@ struct M2LShape {
   static_assert(GAUSS || TT == 16, "32-target tiles use the Gauss scheme");
   // rows per warp: 32 (4 m-tiles) for 16-target tiles; 16 (2 m-tiles) for 32-target
   // tiles, which keeps the accumulators at 48 doubles and halves the W (A operand)
-  // bytes per DMMA -- the L2 -> SM stream of W is what bounds the GEMM
+  // bytes per DMMA.  Measured on config 2: 32-target tiles (1 CTA/SM) 58.9 ms,
+  // 16-target tiles (2 CTAs/SM) 51.9 ms -> only TT = 16 is instantiated
   static constexpr int RW = TT == 32 ? 16 : 32;
   static constexpr int MT = RW / 8;
   static constexpr int THREADS = NPAD / RW * 32;
@@ -552,14 +553,6 @@ void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int
 
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a) {
   if (a.n_item <= 0) return 0;
-  if (tile == 32) {
-    if (n_pad == 32 && n_k == 8) run_gemm<32, 8, 32>(st, a);
-    else if (n_pad == 32 && n_k == 32) run_gemm<32, 32, 32>(st, a);
-    else if (n_pad == 64 && n_k == 64) run_gemm<64, 64, 32>(st, a);
-    else if (n_pad == 128 && n_k == 128) run_gemm<128, 128, 32>(st, a);
-    else return 1;
-    return 0;
-  }
   if (tile != 16) return 1;
   if (n_pad == 32 && n_k == 8) run_gemm<32, 8, 16>(st, a);
   else if (n_pad == 32 && n_k == 32) run_gemm<32, 32, 16>(st, a);

@@ -487,8 +487,6 @@ void build_m2l(Plan& P) {
   } while (0)
   const TreePlan& T = P.T;
   const TreePlan& S = P.S;
-  if (const char* e = std::getenv("FDH_M2L_TILE")) P.prm.tile = std::atoi(e) == 32 ? 32 : 16;  // tuning knob
-  if (!m2l_gauss(P.n_pad)) P.prm.tile = 16;  // 32-target tiles exist for the Gauss shapes only
   const int TT = P.prm.tile;
   // pairs (target slot, key, source slot) grouped by target slot: parallel
   // counting pass, prefix, parallel scatter with atomic cursors (the order
