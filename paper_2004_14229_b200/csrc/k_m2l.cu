@@ -136,13 +136,15 @@ struct M2LShape {
   // so 1; 32-target tiles run 1 CTA/SM and need the overlap
   static constexpr int NBUF = TT == 32 ? 2 : FDH_M2L_NBUF;
   static constexpr int SA = 2 * TT;         // smem accumulator row stride (xor-swizzled columns)
+  static constexpr int SR = NK;             // accumulator rows: W rows >= n_k are zero padding
   // per-key metadata of the item (key id, cnt, same flag, TT source slots and
   // TT target columns) staged in smem windows of MK keys: the per-key loads
   // are off the critical path (they miss L2: each item reads its slice once)
-  static constexpr int MK = 64;
+  static constexpr int MK = GAUSS ? 64 : 16;  // n_pad 224: keeps 2 CTAs/SM
   static constexpr int META = MK * (4 + 1 + 1 + 5 * TT);  // bytes
-  static constexpr size_t SMEM = (size_t)(NBUF * STAGE + NPAD * SA) * sizeof(double) + (META + 15) / 16 * 16;
+  static constexpr size_t SMEM = (size_t)(NBUF * STAGE + SR * SA) * sizeof(double) + (META + 15) / 16 * 16;
   static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(NPAD != 224 || SMEM <= 113 * 1024, "n_pad 224 must keep 2 CTAs/SM");
   // unroll of the k-step-pair loops
   static constexpr int KU = FDH_KUNROLL > 0 ? FDH_KUNROLL : (NPAD <= 128 ? 2 : 1);
   // resident CTAs per SM the register allocation must allow
@@ -314,8 +316,8 @@ __device__ __forceinline__ void m2l_flush(Acc& acc, double* sacc, const uint8_t*
         const int t = j < cnt ? cols[j] : -1;
 #pragma unroll
         for (int mt = 0; mt < S::MT; ++mt) {
-          if (t >= 0) {
-            const int row = rbase + mt * 8;
+          const int row = rbase + mt * 8;
+          if (t >= 0 && row < S::SR) {
             const double p1 = acc.g[0][mt][nt][e], p2 = acc.g[1][mt][nt][e], p3 = acc.g[2][mt][nt][e];
             double* p = sacc + row * S::SA + 2 * (t ^ (row & (TT - 1)));
             p[0] += p1 - p2;
@@ -334,8 +336,8 @@ __device__ __forceinline__ void m2l_flush(Acc& acc, double* sacc, const uint8_t*
       const int t = j < cnt ? cols[j] : -1;
 #pragma unroll
       for (int mt = 0; mt < S::MT; ++mt) {
-        if (t >= 0) {
-          const int row = rbase + mt * 8;
+        const int row = rbase + mt * 8;
+        if (t >= 0 && row < S::SR) {
           double* p = sacc + row * S::SA + 2 * (t ^ (row & (TT - 1)));
           p[0] += acc.o[mt][nt][0];
           p[1] += acc.o[mt][nt][1];
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
   const int item = item0 + (int)blockIdx.x;
   const int64_t k0 = item_k0[item], k1 = item_k1[item];
   // metadata window [w0, w0 + MK)
-  int32_t* m_src = reinterpret_cast<int32_t*>(sacc + NPAD * S::SA);
+  int32_t* m_src = reinterpret_cast<int32_t*>(sacc + S::SR * S::SA);
   int32_t* m_key = m_src + S::MK * TT;
   uint8_t* m_cols = reinterpret_cast<uint8_t*>(m_key + S::MK);
   uint8_t* m_cnt = m_cols + S::MK * TT;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
   };
   load_meta(k0);
 
-  for (int i = threadIdx.x; i < NPAD * S::SA; i += S::THREADS) sacc[i] = 0.0;
+  for (int i = threadIdx.x; i < S::SR * S::SA; i += S::THREADS) sacc[i] = 0.0;
   M2LAcc<MT, S::NG, S::NO> acc;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
     __syncthreads();
   }
   const bool last = seq == nit - 1;
-  for (int idx = threadIdx.x; idx < NPAD * TT; idx += S::THREADS) {
+  for (int idx = threadIdx.x; idx < S::SR * TT; idx += S::THREADS) {  // rows >= n_k of loc stay zero
     const int row = idx / TT, j = idx % TT;
     const int jj = j ^ (row & (TT - 1));
     double2 v = make_double2(sacc[row * S::SA + 2 * jj], sacc[row * S::SA + 2 * jj + 1]);
