@@ -269,7 +269,7 @@ void setup_device(fdh_op* o) {
   }
   const int64_t np2 = 2 * (int64_t)P.n_pad;
   const int64_t nkeys = (int64_t)P.key_level.size();
-  const int64_t wkey = P.n_pad * 3 * (int64_t)P.n_k;  // doubles per coupling matrix ([Re | Im | Re + Im])
+  const int64_t wkey = P.n_pad * m2l_wplanes(P.n_pad) * (int64_t)P.n_k;  // doubles per coupling matrix
   o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
   o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
@@ -373,7 +373,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     } else {
       for (size_t sg = 0; sg < o->segs.size(); ++sg) {
         const auto& S = o->segs[sg];
-        double* slot = o->W + (int64_t)(sg & 1) * o->w_slot_keys * P.n_pad * 3 * (int64_t)P.n_k;
+        double* slot = o->W + (int64_t)(sg & 1) * o->w_slot_keys * P.n_pad * m2l_wplanes(P.n_pad) * (int64_t)P.n_k;
         launch_coupling(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, slot,
                         P.n, P.n_pad, P.n_k, S.key0);
         M2LArgs b = a;

@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
   const double cv[3] = {c[0], c[1], c[2]};
   const double kappa = C->kappa;
   __syncthreads();
-  double* Wk = W + (key - wbase) * n_pad * 3 * n_k;
+  const int np = m2l_wplanes(n_pad);
+  double* Wk = W + (key - wbase) * n_pad * np * n_k;
   for (int idx = threadIdx.x; idx < kCplRows * n_k; idx += blockDim.x) {
     const int j = r0 + idx / n_k, k = idx % n_k;
     if (j >= n_pad) continue;
@@ -87,9 +88,9 @@ __global__ void __launch_bounds__(256) k_coupling(const Consts* __restrict__ C, 
     // k-interleaved within blocks of 8 (k = 8b + 4h + q stored at 8b + 2q + h), so
     // that a lane's A fragments of two consecutive k-steps are one 16-byte load
     const int kp = (k & ~7) | ((k & 3) << 1) | ((k >> 2) & 1);
-    Wk[(int64_t)j * 3 * n_k + kp] = re;
-    Wk[(int64_t)j * 3 * n_k + n_k + kp] = im;
-    Wk[(int64_t)j * 3 * n_k + 2 * n_k + kp] = re + im;  // Gauss plane
+    Wk[(int64_t)j * np * n_k + kp] = re;
+    Wk[(int64_t)j * np * n_k + n_k + kp] = im;
+    if (np == 3) Wk[(int64_t)j * np * n_k + 2 * n_k + kp] = re + im;  // Gauss plane
   }
 }
 
@@ -111,7 +112,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int NPAD, int NK, int TT>
 struct M2LShape {
-  static constexpr int K3 = 3 * NK;         // W row length: [Re A | Im A | Re A + Im A]
+  static constexpr int K3 = m2l_wplanes(NPAD) * NK;  // W row length: [Re A | Im A (| Re A + Im A)]
   static constexpr int GS = 2 * NPAD;       // moment slot stride in HBM ([Re | Im] planes of NPAD)
   // smem moment column: [Re (NK) | pad | Im (NK) | pad], IMOFF == 8 and MS == 4 (mod 16):
   // both B-fragment patterns (4 columns x Re/Im x 4 k, and 4 columns x 4 k per

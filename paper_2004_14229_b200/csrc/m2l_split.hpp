@@ -19,6 +19,8 @@ struct M2LSplit {
 };
 // the Gauss scheme is used for n_pad <= 128 (k_m2l_gemm: register budget)
 FDH_HD constexpr bool m2l_gauss(int n_pad) { return n_pad <= 128; }
+// planes of a coupling matrix row: [Re A | Im A] (+ Re A + Im A for the Gauss shapes)
+FDH_HD constexpr int m2l_wplanes(int n_pad) { return m2l_gauss(n_pad) ? 3 : 2; }
 FDH_HD inline M2LSplit m2l_split(int cnt, bool gauss) {
   if (!gauss) return {0, (cnt + 3) >> 2};
   const int r = cnt & 7;  // remainder after full 8-target Gauss n-tiles
