@@ -29,14 +29,25 @@
 #ifndef FDH_KUNROLL
 #define FDH_KUNROLL 0
 #endif
-#ifndef FDH_M2L_NBUF
-#define FDH_M2L_NBUF 1
+#ifndef FDH_M2L_TRACE
+#define FDH_M2L_TRACE 0
 #endif
 #ifndef FDH_M2L_MINB
 #define FDH_M2L_MINB 0
 #endif
 
 namespace fdhelm {
+
+#if FDH_M2L_TRACE
+// debug build only: per-phase SM cycles of warp 0 of every M2L CTA
+__device__ unsigned long long g_m2l_trace[8];
+#define FDH_TR_T(v) const long long v = clock64()
+#define FDH_TR_ADD(i, d) \
+  if (threadIdx.x == 0) atomicAdd(&g_m2l_trace[i], (unsigned long long)(d))
+#else
+#define FDH_TR_T(v)
+#define FDH_TR_ADD(i, d)
+#endif
 
 namespace {
 
@@ -109,7 +120,6 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
-
 template <int NPAD, int NK, int TT>
 struct M2LShape {
   static constexpr int K3 = m2l_wplanes(NPAD) * NK;  // W row length: [Re A | Im A (| Re A + Im A)]
@@ -131,11 +141,11 @@ struct M2LShape {
   static constexpr int RW = TT == 32 ? 16 : 32;
   static constexpr int MT = RW / 8;
   static constexpr int THREADS = NPAD / RW * 32;
+  static_assert(THREADS % TT == 0, "whole threads per staged column");
   static constexpr int STAGE = TT * MS;     // doubles per smem stage
-  // moment stages: 2 overlaps the staging of key k+1 with the DMMAs of key k.
-  // 16-target tiles: measured 10 % slower on config 2 (55 -> 61 ms, 2 CTAs/SM),
-  // so 1; 32-target tiles run 1 CTA/SM and need the overlap
-  static constexpr int NBUF = TT == 32 ? 2 : FDH_M2L_NBUF;
+  // one moment stage: double-buffering (staging key k+1 during key k) measured
+  // 10 % slower on config 2 (51.9 -> 58.9 ms at 2 CTAs/SM)
+  static constexpr int NBUF = 1;
   static constexpr int SA = 2 * TT;         // smem accumulator row stride (xor-swizzled columns)
   static constexpr int SR = NK;             // accumulator rows: W rows >= n_k are zero padding
   // per-key metadata of the item (key id, cnt, same flag, TT source slots and
@@ -166,21 +176,31 @@ struct M2LAcc {
   double o[MT][NO][2];
 };
 
-// stage the moments of the first ncol compacted columns (cnt valid, rest zero)
+// stage the moments of the first ncol compacted columns (cnt valid, rest zero).
+// THREADS / TT threads per column: one smem read of the source slot and one
+// base address per thread, then a strided run of 16-byte cp.async.  (Bulk copies
+// on the TMA engine with an mbarrier measured slower: 52.1-52.4 vs 51.3 ms.)
 template <int NPAD, int NK, int TT>
 __device__ __forceinline__ void m2l_stage(double* buf, const int32_t* __restrict__ src, int cnt, int ncol,
                                           const double* __restrict__ mom) {
   using S = M2LShape<NPAD, NK, TT>;
-  constexpr int CH = NK / 2;  // 16-byte chunks per plane
-  for (int idx = threadIdx.x; idx < ncol * 2 * CH; idx += S::THREADS) {
-    const int c = idx / (2 * CH), ch = idx % (2 * CH);
-    const int im = ch >= CH, e = 2 * (ch - im * CH);
-    double* dst = buf + c * S::MS + (im ? S::IMOFF : 0) + e;
-    if (c < cnt) {
-      cp_async16(dst, mom + (int64_t)src[c] * S::GS + (im ? NPAD : 0) + e);
-    } else {
-      dst[0] = 0.0;
-      dst[1] = 0.0;
+  constexpr int CH = NK / 2;             // 16-byte chunks per plane
+  constexpr int TPC = S::THREADS / TT;   // threads per column
+  const int c = threadIdx.x / TPC, t = threadIdx.x % TPC;
+  if (c >= ncol) return;
+  double* dst = buf + c * S::MS;
+  if (c < cnt) {
+    const double* g = mom + (int64_t)src[c] * S::GS;
+#pragma unroll 4
+    for (int ch = t; ch < 2 * CH; ch += TPC) {
+      const int im = ch >= CH, e = 2 * (ch - im * CH);
+      cp_async16(dst + (im ? S::IMOFF : 0) + e, g + (im ? NPAD : 0) + e);
+    }
+  } else {
+    for (int ch = t; ch < 2 * CH; ch += TPC) {
+      const int im = ch >= CH, e = 2 * (ch - im * CH);
+      dst[(im ? S::IMOFF : 0) + e] = 0.0;
+      dst[(im ? S::IMOFF : 0) + e + 1] = 0.0;
     }
   }
 }
@@ -443,8 +463,9 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
   const double* __restrict__ Wrow = W + (int64_t)(warp * S::RW + (lane >> 2)) * S::K3 + 2 * bk;
   double2 a[MT];
   if constexpr (S::PF) m2l_lda<S::K3, MT>(a, Wrow + ((int64_t)m_key[0] - key_base) * NPAD * S::K3);
-  int stage = 0;
+  FDH_TR_T(t_loop);
   for (int64_t kk = k0; kk < k1; ++kk) {
+    FDH_TR_T(t0);
     if (kk + 1 < k1 && kk + 1 - w0 >= S::MK) {  // slide the window to [kk - 1, ...)
       __syncthreads();
       w0 = kk - 1;
@@ -452,37 +473,37 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
     }
     const int j = (int)(kk - w0);
     const int cnt = m_cnt[j];
-    if constexpr (S::NBUF == 2) {  // stage key kk+1 into the other buffer, wait for key kk
-      if (kk + 1 < k1) {
-        const int cn = m_cnt[j + 1];
-        m2l_stage<NPAD, NK, TT>(smem + (stage ^ 1) * S::STAGE, m_src + (j + 1) * TT, cn,
-                                m2l_ncol(m2l_split(cn, S::GAUSS)), mom);
-      }
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<0>();  // moments of key kk landed (this thread's copies; the barrier covers the rest)
     __syncthreads();
+    FDH_TR_T(t1);
     if (kk > k0 && !m_same[j]) m2l_flush<NPAD, NK, TT>(acc, sacc, m_cols + (j - 1) * TT, m_cnt[j - 1], warp, lane);
-    const double* Bst = smem + stage * S::STAGE;
+    FDH_TR_T(t2);
+    const double* Bst = smem;
     const double* Bg = Bst + (lane >> 2) * S::MS + bk;
     const M2LSplit sp = m2l_split(cnt, S::GAUSS);
     const double* Bo = Bst + (8 * sp.a3 + bcol) * S::MS + bk;
     const double* __restrict__ Wk = Wrow + ((int64_t)m_key[j] - key_base) * NPAD * S::K3;
     const double* __restrict__ Wn = kk + 1 < k1 ? Wrow + ((int64_t)m_key[j + 1] - key_base) * NPAD * S::K3 : nullptr;
     m2l_key_dispatch<NPAD, NK, TT>(sp, acc, a, Wk, Wn, Bg, Bo, re_off, im_off, sgn);
+    FDH_TR_T(t3);
     __syncthreads();
-    if constexpr (S::NBUF == 2) {
-      stage ^= 1;
-    } else {
-      if (kk + 1 < k1) {
-        const int cn = m_cnt[j + 1];
-        m2l_stage<NPAD, NK, TT>(smem, m_src + (j + 1) * TT, cn, m2l_ncol(m2l_split(cn, S::GAUSS)), mom);
-      }
-      cp_async_commit();
+    FDH_TR_T(t4);
+    if (kk + 1 < k1) {
+      const int cn = m_cnt[j + 1];
+      m2l_stage<NPAD, NK, TT>(smem, m_src + (j + 1) * TT, cn, m2l_ncol(m2l_split(cn, S::GAUSS)), mom);
     }
+    cp_async_commit();
+    FDH_TR_T(t5);
+    FDH_TR_ADD(0, t1 - t0);  // wait for the staged moments + barrier
+    FDH_TR_ADD(1, t2 - t1);  // flush
+    FDH_TR_ADD(2, t3 - t2);  // DMMA key loop
+    FDH_TR_ADD(3, t4 - t3);  // end-of-key barrier
+    FDH_TR_ADD(4, t5 - t4);  // staging issue
+    FDH_TR_ADD(6, 1);        // keys
   }
+  FDH_TR_T(t_end);
+  FDH_TR_ADD(5, t_end - t_loop);
+  FDH_TR_ADD(7, 1);  // items
   m2l_flush<NPAD, NK, TT>(acc, sacc, m_cols + (k1 - 1 - w0) * TT, m_cnt[k1 - 1 - w0], warp, lane);
   __syncthreads();
   // ---- chained accumulation into the tile (chunk order)
@@ -568,3 +589,15 @@ int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs
 }
 
 }  // namespace fdhelm
+
+#if FDH_M2L_TRACE
+extern "C" int fdh_debug_m2l_trace(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, fdhelm::g_m2l_trace, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(fdhelm::g_m2l_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
