@@ -80,6 +80,7 @@ struct fdh_op {
   };
   std::vector<Seg> segs;
   int64_t w_slot_keys = 0;
+  double2* sctab = nullptr;  // (sin, cos)(i pi / 256), i < 512: near-field table sincos
   double2 *q = nullptr, *q4 = nullptr, *yslot = nullptr, *xin = nullptr, *yout = nullptr;
   int* flag = nullptr;
   bool timing = false;
@@ -276,6 +277,15 @@ void setup_device(fdh_op* o) {
   o->ticket = o->alloc<int>((size_t)std::max(o->n_tile, 1));
   o->q = o->alloc<double2>((size_t)o->ns);
   o->q4 = o->alloc<double2>((size_t)o->ns);
+  {
+    std::vector<double2> tab(512);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int i = 0; i < 512; ++i) {
+      const long double a = (long double)i * pi / 256.0L;
+      tab[i] = make_double2((double)sinl(a), (double)cosl(a));
+    }
+    o->sctab = o->up(tab);
+  }
   o->yslot = o->alloc<double2>((size_t)o->nt);
   o->ynear = o->alloc<double2>((size_t)o->nt);
   o->xin = o->alloc<double2>((size_t)o->ns);
@@ -398,7 +408,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
   launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
              o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
-             o->kappa * P.nf_max_dist);
+             o->kappa * P.nf_max_dist, o->sctab);
   L += o->n_leaf > 0;
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
   if (o->overlap_nf) CK(cudaEventRecord(o->ev_nf, o->st2));

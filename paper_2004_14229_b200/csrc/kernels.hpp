@@ -31,7 +31,7 @@ void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg,
                 const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
                 const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
                 const double2* q4, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
-                double2* y_slot, int* flag, double max_phase);
+                double2* y_slot, int* flag, double max_phase, const double2* sctab);
 
 // ---- k_m2l.cu
 void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
