@@ -138,7 +138,7 @@ struct M2LShape {
   // tiles, which keeps the accumulators at 48 doubles and halves the W (A operand)
   // bytes per DMMA.  Measured on config 2: 32-target tiles (1 CTA/SM) 58.9 ms,
   // 16-target tiles (2 CTAs/SM) 51.9 ms -> only TT = 16 is instantiated
-  static constexpr int RW = TT == 32 ? 16 : 32;
+  static constexpr int RW = (TT == 32 || (GAUSS && NPAD > 128)) ? 16 : 32;
   static constexpr int MT = RW / 8;
   static constexpr int THREADS = NPAD / RW * 32;
   static_assert(THREADS % TT == 0, "whole threads per staged column");
@@ -151,15 +151,15 @@ struct M2LShape {
   // per-key metadata of the item (key id, cnt, same flag, TT source slots and
   // TT target columns) staged in smem windows of MK keys: the per-key loads
   // are off the critical path (they miss L2: each item reads its slice once)
-  static constexpr int MK = GAUSS ? 64 : 16;  // n_pad 224: keeps 2 CTAs/SM
+  static constexpr int MK = (GAUSS || NPAD != 224) ? 64 : 16;  // real-GEMM n_pad 224: keeps 2 CTAs/SM
   static constexpr int META = MK * (4 + 1 + 1 + 5 * TT);  // bytes
   static constexpr size_t SMEM = (size_t)(NBUF * STAGE + SR * SA) * sizeof(double) + (META + 15) / 16 * 16;
   static_assert(SMEM <= 227 * 1024, "shared memory");
-  static_assert(NPAD != 224 || SMEM <= 113 * 1024, "n_pad 224 must keep 2 CTAs/SM");
+  static_assert(GAUSS || NPAD != 224 || SMEM <= 113 * 1024, "real-GEMM n_pad 224 must keep 2 CTAs/SM");
   // unroll of the k-step-pair loops
   static constexpr int KU = FDH_KUNROLL > 0 ? FDH_KUNROLL : (NPAD <= 128 ? 2 : 1);
   // resident CTAs per SM the register allocation must allow
-  static constexpr int MINB = FDH_M2L_MINB > 0 ? FDH_M2L_MINB : (NPAD == 224 ? 2 : 1);
+  static constexpr int MINB = FDH_M2L_MINB > 0 ? FDH_M2L_MINB : (NPAD == 224 && !GAUSS ? 2 : 1);
   static constexpr int NG = GAUSS ? TT / 8 : 1;  // Gauss n-tiles held (1 = unused)
   static constexpr int NO = GAUSS ? 1 : TT / 4;  // real-GEMM n-tiles held
   // A fragments prefetched one k-step pair ahead in registers (Gauss shapes;

@@ -2,6 +2,10 @@
 // k_m2l_gemm (scheme dispatch).
 #pragma once
 
+#ifndef FDH_GAUSS_MAX_NPAD
+#define FDH_GAUSS_MAX_NPAD 224
+#endif
+
 namespace fdhelm {
 
 #ifdef __CUDACC__
@@ -18,7 +22,7 @@ struct M2LSplit {
   int a3, ao;
 };
 // the Gauss scheme is used for n_pad <= 128 (k_m2l_gemm: register budget)
-FDH_HD constexpr bool m2l_gauss(int n_pad) { return n_pad <= 128; }
+FDH_HD constexpr bool m2l_gauss(int n_pad) { return n_pad <= FDH_GAUSS_MAX_NPAD; }
 // planes of a coupling matrix row: [Re A | Im A] (+ Re A + Im A for the Gauss shapes)
 FDH_HD constexpr int m2l_wplanes(int n_pad) { return m2l_gauss(n_pad) ? 3 : 2; }
 FDH_HD inline M2LSplit m2l_split(int cnt, bool gauss) {
