@@ -285,7 +285,12 @@ def run_ours(args, c, rank, world, local_rank):
                      "peak_source": "measured live: fdh_fp64_peak_tflops(0) DMMA microbenchmark (no FP64 entry in "
                                     "MEASURED_PEAKS.json)",
                      "algorithmic": f"8 n^2 flop per admissible block x N_C={st['n_c']} = {m2l_flops:.4g} flop per "
-                                    f"launch; executed incl. padding/empty columns {st['m2l_flops_executed']:.4g}",
+                                    f"launch (SURVEY.md 8(d); the count holds for a 3M complex product)",
+                     "issued_flop": st["m2l_flops_executed"],
+                     "issued_frac": (st["m2l_flops_executed"] / (gemm_ms * 1e-3) / 1e12 / peak
+                                     if (gemm_ms > 0 and peak) else None),
+                     "issued_note": "flop the kernel issues on DMMA: Gauss 3-multiplication product (6 n^2) for "
+                                    "8-target n-tiles, 8 n^2 real GEMM for <= 4, incl. padding columns",
                      "gemm_ms": gemm_ms, "share_of_step": gemm_ms / ms_per_step if ms_per_step else None},
         "phases_ms": ph,
         "p2p": {"pairs": st["m_d"], "ms": p2p_ms,

@@ -61,14 +61,17 @@ def test_cfg5_shape_nonuniform():
     assert oracle.rel_l2(y, yo) <= TOL
 
 
-def test_pure_nearfield_and_dense():
+@pytest.mark.parametrize("kappa,eta2", [(1e6, 1.0), (5e5, 1e-9), (57.0, 1e-9), (1.0, 1e-9)])
+def test_pure_nearfield_and_dense(kappa, eta2):
+    # near-field phase kappa * d_max (d_max ~ sqrt 3) selects the P2P variant:
+    # > 1.5e6 library sincos, < 1.5e6 exact r + fast sincos, <= 100 FMA r + table sincos
     rng = np.random.default_rng(11)
     pt = [rng.random(900) for _ in range(3)]
     ps = [rng.random(700) for _ in range(3)]
     q = rng.standard_normal(700) + 1j * rng.standard_normal(700)
-    op = F.DirectionalOperator(pt, ps, (0, 0, 0), (1, 1, 1), 1e6, n_max=16, m=2)
+    op = F.DirectionalOperator(pt, ps, (0, 0, 0), (1, 1, 1), kappa, n_max=16, m=2, eta2=eta2)
     assert op.stats()["n_c"] == 0
-    yd = oracle.dense_rows(pt, ps, q, 1e6, np.arange(900))
+    yd = oracle.dense_rows(pt, ps, q, kappa, np.arange(900))
     assert oracle.rel_l2(op.apply(q), yd) <= 1e-13
 
 
