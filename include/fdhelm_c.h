@@ -86,6 +86,8 @@ typedef struct fdh_stats {
   int64_t gpu_structure;        /* 1: built by the k_setup.cu kernels         */
   int64_t w_resident;           /* 1: coupling matrices kept in HBM           */
   int64_t w_segments;           /* else: per-apply generation segments        */
+  int64_t m2l_impl;             /* 0: FP64 DMMA (mma.sync), 1: int8 tcgen05 digit products */
+  int64_t m2l_i8_ops;           /* int8 tensor ops (2 per MAC) issued by one M2L (impl 1)  */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

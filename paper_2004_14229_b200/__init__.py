@@ -42,7 +42,7 @@ class FdhStats(C.Structure):
                 ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
                 ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
                 ("structure_ms", C.c_double), ("gpu_structure", C.c_int64), ("w_resident", C.c_int64),
-                ("w_segments", C.c_int64)]
+                ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64)]
 
 
 class FdhError(RuntimeError):

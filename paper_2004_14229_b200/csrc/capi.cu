@@ -72,6 +72,12 @@ struct fdh_op {
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
   double *W = nullptr, *mom = nullptr, *loc = nullptr;
+  // int8 tensor-core M2L (k_m2l_i8.cu): digits of W (setup) and of the moments (per apply)
+  bool i8 = false;
+  int nkq = 0;
+  int8_t *Wq = nullptr, *Mq = nullptr;
+  unsigned long long *lvmax_w = nullptr, *lvmax_v = nullptr;
+  int32_t *tile_level_d = nullptr, *s_slot_level = nullptr;
   // on-the-fly coupling (W does not fit): segments of consecutive key chunks, 2-slot ring
   bool w_resident = true;
   struct Seg {
@@ -295,6 +301,32 @@ void setup_device(fdh_op* o) {
   // memory), else generated per apply in segments of key chunks (config 4: 240 GB)
   size_t fre = 0, tot = 0;
   CK(cudaMemGetInfo(&fre, &tot));
+  if (P.prm.m2l_impl == 1) {
+    // int8 digits of every coupling matrix, resident (k_m2l_i8.cu); per-level
+    // scales from a first generation pass, digits from a second
+    o->i8 = true;
+    o->nkq = (P.n + 15) / 16 * 16;
+    const int64_t wq = m2l_i8_wbytes_per_key(P.n, o->nkq) * nkeys;
+    const int64_t mq = m2l_i8_mbytes_per_slot(o->nkq) * P.S.nslots;
+    if ((double)(wq + mq) > 0.7 * (double)fre) throw PlanError{-1, "int8 coupling digits do not fit"};
+    o->Wq = o->alloc<int8_t>((size_t)std::max<int64_t>(wq, 16));
+    o->Mq = o->alloc<int8_t>((size_t)std::max<int64_t>(mq, 16));
+    o->lvmax_w = o->alloc<unsigned long long>(kMaxLevels);
+    o->lvmax_v = o->alloc<unsigned long long>(kMaxLevels);
+    CK(cudaMemsetAsync(o->Wq, 0, (size_t)std::max<int64_t>(wq, 16), o->st));
+    CK(cudaMemsetAsync(o->Mq, 0, (size_t)std::max<int64_t>(mq, 16), o->st));
+    CK(cudaMemsetAsync(o->lvmax_w, 0, sizeof(unsigned long long) * kMaxLevels, o->st));
+    o->tile_level_d = o->up(P.tile_level);
+    o->s_slot_level = o->up(P.S.slot_level);
+    const int64_t chunk = 4096;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+        launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
+                           o->key_dir, pass, o->lvmax_w, o->Wq, P.n, o->nkq);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(o->st));
+    return;
+  }
   const double wbytes = 8.0 * (double)wkey * (double)nkeys;
   const char* otf = std::getenv("FDH_W_ONTHEFLY");
   o->w_resident = !(otf && otf[0] == '1') && wbytes <= 0.7 * (double)fre;
@@ -355,7 +387,38 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   rec(o, FDH_PHASE_M2L, st);
   if (o->overlap_nf) CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(P.T.nslots * 2 * np), st));
-  if (o->n_item > 0) {
+  if (o->n_item > 0 && o->i8) {
+    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
+    launch_mom_quant(st, o->mom, o->s_slot_level, P.S.nslots, n, np, o->nkq, o->lvmax_v, o->Mq);
+    M2LI8Args a;
+    a.n_item = o->n_item;
+    a.item_tile = o->item_tile;
+    a.item_seq = o->item_seq;
+    a.item_k0 = o->item_k0;
+    a.item_k1 = o->item_k1;
+    a.tile_nitem = o->tile_nitem;
+    a.tile_tslot = o->tile_tslot;
+    a.tile_level = o->tile_level_d;
+    a.tile_keys = o->tile_keys;
+    a.tile_src = o->tile_src;
+    a.tile_cols = o->tile_cols;
+    a.tile_cnt = o->tile_cnt;
+    a.Wq = o->Wq;
+    a.Mq = o->Mq;
+    a.lvmax_w = o->lvmax_w;
+    a.lvmax_v = o->lvmax_v;
+    a.tile_acc = o->tile_acc;
+    a.ticket = o->ticket;
+    a.loc = o->loc;
+    a.err = o->flag;
+    a.nkq = o->nkq;
+    a.n_pad = np;
+    a.fkeys = P.prm.m2l_fkeys;
+    rec(o, FDH_NPHASES + 1, st);
+    if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+    rec(o, FDH_NPHASES + 2, st);
+    L += 3;
+  } else if (o->n_item > 0) {
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
     M2LArgs a;
     a.n_item = o->n_item;
@@ -518,8 +581,34 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     prm.gpu_structure = device && !(hs && hs[0] == '1');
     o->rank = rank;
     o->world = world;
+    // M2L implementation: the int8 tcgen05 kernel where it is compiled (n <= 256
+    // nodes per box, i.e. m <= 5), FP64 DMMA otherwise; FDH_M2L_IMPL=dmma|i8 overrides
+    const int nbox = (m + 1) * (m + 1) * (m + 1);
+    const char* mi = std::getenv("FDH_M2L_IMPL");
+    const bool want_i8 = device && m >= 1 && nbox <= 256 && !(mi && std::string(mi) == "dmma");
+    if (want_i8) {
+      prm.m2l_impl = 1;
+      prm.tile = nbox <= 128 ? 32 : 16;
+      prm.m2l_fkeys = m2l_i8_fkeys((nbox + 15) / 16 * 16);
+    }
     build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
-    if (device) setup_device(o);
+    if (device) {
+      try {
+        setup_device(o);
+      } catch (const PlanError& e) {
+        if (e.code != -1) throw;
+        // int8 digits do not fit: rebuild with the FP64 DMMA path
+        delete o;
+        o = new fdh_op;
+        o->rank = rank;
+        o->world = world;
+        prm.m2l_impl = 0;
+        prm.tile = 16;
+        prm.m2l_fkeys = 0;
+        build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
+        setup_device(o);
+      }
+    }
     o->stats.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   });
   if (rc != FDH_OK) {
@@ -641,6 +730,13 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->w_segments = (int64_t)o->segs.size();
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
+  s->m2l_impl = o->i8 ? 1 : 0;
+  if (o->i8) {
+    // int8 MACs issued by k_m2l_i8: per (tile, key) and K byte: 128 rows x sum_i (KS - i) 2 TT columns per m-block
+    const int64_t cols = (int64_t)kI8Digits * (kI8Digits + 1) / 2 * 2 * P.prm.tile;
+    s->m2l_flops_executed = 0;
+    s->m2l_i8_ops = 2 * (int64_t)P.tile_keys.size() * ((P.n + 127) / 128) * 128 * (2 * (int64_t)o->nkq) * cols;
+  }
   return FDH_OK;
 }
 

@@ -1,0 +1,552 @@
+// k_m2l_i8.cu -- M2L on the 5th-generation tensor cores (tcgen05.mma kind::i8, sm_100a).
+//
+// M2L is g~_{t,c} += A_{c,t x s} v~_{s,c} over the admissible
+// leaves; per tile of TT target slots and coupling key it is the real GEMM
+//
+//     C[n x 2TT] = W[n x KP] * B[KP x 2TT],  W = [Re A | Im A],
+//     B(:, 2j) = [Re v_j ; -Im v_j],  B(:, 2j+1) = [Im v_j ; Re v_j]      (KP = 2 n_kq)
+//
+// in complex128.  tcgen05 has no f64 kind, so the FP64 product is computed
+// EXACTLY in integers (Ozaki-style fixed-point slicing):
+//   * W (per tree level, one power-of-two scale S_W = 2^(eW+1) > 2 max|W|) and the
+//     moments v (per level, S_V) are rounded to 7*KS-bit fixed point and split
+//     into KS balanced base-128 digits d_i in [-64, 64] (int8), most significant
+//     first: x = S * sum_i d_i 2^(-7(i+1)) (+ rounding error <= S 2^(-7 KS - 1));
+//   * the product needs only the digit pairs i + j <= LMAX = KS - 1 (the dropped
+//     pairs weigh <= 2^(-7(KS+1)) relative); pairs of one level L = i + j share
+//     the weight 2^(-7(L+2)) and are summed EXACTLY in one int32 TMEM accumulator
+//     column block: one MMA per W digit i multiplies W_i by the B digits
+//     [B_0 | B_1 | ... | B_{LMAX-i}] stacked along N and lands in the level
+//     blocks i .. LMAX (D column = L * 2TT + target column);
+//   * every key of a (tile, key-chunk) item accumulates into the same TMEM
+//     columns (the scales are per level, hence per tile), so the int32 sums are
+//     exact as long as an item has <= F keys (F from the digit bound, planner);
+//   * the epilogue reads TMEM once per item and forms sum_L acc_L 2^(-7(L+2))
+//     S_W S_V in FP64 (fixed order); items of a tile are chained in key-chunk
+//     order as in k_m2l_gemm (deterministic, no FP atomics).
+// Relative error per block ~1e-14 at KS = 7 (vs 1e-12 allowed, north_star):
+// the product is exact, only the 7*KS-bit rounding of W and v and the dropped
+// digit pairs remain.
+//
+// Data movement: the digits of W live in HBM pre-arranged in the UMMA canonical
+// K-major layout (core matrices of 8 rows x 16 B, SWIZZLE_NONE), one contiguous
+// block per (key, K chunk of 32), moved by ONE cp.async.bulk (TMA engine) per
+// pipeline stage onto an mbarrier; the moment digits of the (up to TT) source
+// slots of a key are gathered by all threads with 16-byte cp.async.  A single
+// thread issues the MMAs (UTCIMMA) and commits them to the stage's "empty"
+// mbarrier; NST stages in flight.
+#include "kernels.hpp"
+
+#include <algorithm>
+
+namespace fdhelm {
+
+namespace {
+
+constexpr int kI8Threads = 128;
+constexpr int kGather = 64;           // threads (warps 2-3) gathering the moment digits
+constexpr int kKC = 32;               // K bytes per MMA k-step / pipeline stage
+constexpr int kCore = 128 * kKC;      // bytes of one 128-row x 32-byte operand block
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// UMMA shared-memory descriptor, K-major SWIZZLE_NONE: LBO = stride between the
+// two 16-byte K core matrices (128 B), SBO = stride between 8-row groups (256 B);
+// verified on the B200 by tools/umma_i8_probe.cu
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// byte offset of element (row r, k) in a 128 x 32 K-major core-matrix block
+__host__ __device__ __forceinline__ int core_off(int r, int k) {
+  return ((r >> 3) * 2 + (k >> 4)) * 128 + (r & 7) * 16 + (k & 15);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- digits
+// x -> KS balanced base-128 digits (most significant first) of rint(x / S 2^(7 KS)),
+// S = 2^(ex + 1) > 2 |x|.  Exact integer arithmetic after one rounding.
+template <int KS>
+__device__ __forceinline__ void to_digits(double x, int ex, int8_t (&d)[KS]) {
+  long long X = __double2ll_rn(ldexp(x, 7 * KS - ex - 1));
+#pragma unroll
+  for (int i = KS - 1; i > 0; --i) {
+    const long long r = ((X + 64) & 127) - 64;
+    d[i] = (int8_t)r;
+    X = (X - r) >> 7;
+  }
+  d[0] = (int8_t)X;
+}
+__device__ __forceinline__ int level_exp(const unsigned long long* lvmax, int l) {
+  int ex = 0;
+  frexp(__longlong_as_double((long long)lvmax[l]), &ex);
+  return ex;
+}
+
+// per-level max |Re|, |Im| of the coupling matrices (pass 0) and their digits
+// (pass 1), in the canonical frame of k_coupling; entries are
+// computed exactly as there.
+constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // geometry.hpp:11
+constexpr int kCplRows = 8;
+template <int KS>
+__global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ C, const double* __restrict__ dirtab,
+                                                     int64_t key0, const int32_t* __restrict__ key_level,
+                                                     const int64_t* __restrict__ key_d,
+                                                     const int32_t* __restrict__ key_dir, int pass,
+                                                     unsigned long long* __restrict__ lvmax, int8_t* __restrict__ Wq,
+                                                     int n, int nkq, int mb) {
+  __shared__ double tn[3][kMaxP], sn[3][kMaxP];
+  __shared__ double red[8];
+  const int64_t key = key0 + blockIdx.x;
+  const int r0 = blockIdx.y * kCplRows;
+  const int p = C->p;
+  const int l = key_level[key];
+  if (threadIdx.x < 3 * p) {
+    const int a = threadIdx.x / p, nu = threadIdx.x % p;
+    const double side = C->side_t[l][a];
+    const int64_t d = key_d[3 * key + a];
+    tn[a][nu] = cheb_node(__dmul_rn((double)d, side), __dmul_rn((double)(d + 1), side), C->cheb_cos[nu]);
+    sn[a][nu] = cheb_node(0.0, __dmul_rn(1.0, side), C->cheb_cos[nu]);
+  }
+  const double* c = dir_vec(C, dirtab, l, key_dir[key]);
+  const double cv[3] = {c[0], c[1], c[2]};
+  const double kappa = C->kappa;
+  __syncthreads();
+  const int ex = pass ? level_exp(lvmax, l) : 0;
+  const int nch = 2 * nkq / kKC;
+  double mx = 0.0;
+  for (int idx = threadIdx.x; idx < kCplRows * n; idx += blockDim.x) {
+    const int j = r0 + idx / n, k = idx % n;
+    if (j >= n) continue;
+    const double d[3] = {__dsub_rn(tn[0][j / (p * p)], sn[0][k / (p * p)]),
+                         __dsub_rn(tn[1][(j / p) % p], sn[1][(k / p) % p]),
+                         __dsub_rn(tn[2][j % p], sn[2][k % p])};
+    const double r = sqrt(dot3(d, d));  // geometry.hpp:92-98
+    const double ph = __dmul_rn(kappa, __dsub_rn(r, dot3(d, cv)));
+    const double w = __ddiv_rn(1.0, __dmul_rn(kFourPi, r));
+    double s, co;
+    sincos(ph, &s, &co);
+    const double re = __dmul_rn(w, co), im = __dmul_rn(w, s);
+    if (!pass) {
+      mx = fmax(mx, fmax(fabs(re), fabs(im)));
+      continue;
+    }
+    int8_t dr[KS], di[KS];
+    to_digits<KS>(re, ex, dr);
+    to_digits<KS>(im, ex, di);
+    const int b = j >> 7, rr = j & 127;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = h ? nkq + k : k;  // K index: [Re A | Im A]
+      const int ch = kk / kKC, kin = kk % kKC;
+      int8_t* base = Wq + ((key * nch + ch) * KS * mb + b) * (int64_t)kCore + core_off(rr, kin);
+#pragma unroll
+      for (int i = 0; i < KS; ++i) base[(int64_t)i * mb * kCore] = h ? di[i] : dr[i];
+    }
+  }
+  if (!pass) {
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+      atomicMax(lvmax + l, (unsigned long long)__double_as_longlong(mx));
+    }
+  }
+}
+
+// moments: per-level max (pass 0), then digits of every source slot (pass 1):
+// Mq: per (slot, K chunk of 32) one contiguous block of KS x 2 (kb) x 2 (h) x 16 B
+// = the pieces a gather warp copies with consecutive lanes; digit i of row h,
+// h = 0: [Re v | -Im v], h = 1: [Im v | Re v] (K index kk < n_kq: first half)
+__device__ __forceinline__ int64_t mq_off(int64_t slot, int nch, int i, int h, int kk) {
+  const int ch = kk / kKC, kin = kk % kKC;
+  return (slot * nch + ch) * (int64_t)(kI8Digits * 4 * 16) + ((i * 2 + (kin >> 4)) * 2 + h) * 16 + (kin & 15);
+}
+__global__ void __launch_bounds__(128) k_mom_max(const double* __restrict__ mom, const int32_t* __restrict__ slot_level,
+                                                 int n, int n_pad, unsigned long long* __restrict__ lvmax) {
+  __shared__ double red[4];
+  const int64_t s = blockIdx.x;
+  const double* g = mom + s * 2 * n_pad;
+  double mx = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) mx = fmax(mx, fmax(fabs(g[k]), fabs(g[n_pad + k])));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mx = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+    if (mx > 0.0) atomicMax(lvmax + slot_level[s], (unsigned long long)__double_as_longlong(mx));
+  }
+}
+template <int KS>
+__global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mom,
+                                                   const int32_t* __restrict__ slot_level,
+                                                   const unsigned long long* __restrict__ lvmax, int n, int n_pad,
+                                                   int nkq, int8_t* __restrict__ Mq) {
+  const int64_t s = blockIdx.x;
+  const double* g = mom + s * 2 * n_pad;
+  const int ex = level_exp(lvmax, slot_level[s]);
+  const int kp = 2 * nkq;
+  const int nch = kp / kKC;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    int8_t dr[KS], di[KS];
+    to_digits<KS>(g[k], ex, dr);
+    to_digits<KS>(g[n_pad + k], ex, di);
+#pragma unroll
+    for (int i = 0; i < KS; ++i) {
+      Mq[mq_off(s, nch, i, 0, k)] = dr[i];
+      Mq[mq_off(s, nch, i, 0, nkq + k)] = (int8_t)(-di[i]);
+      Mq[mq_off(s, nch, i, 1, k)] = di[i];
+      Mq[mq_off(s, nch, i, 1, nkq + k)] = dr[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- M2L
+template <int MB, int TT, int KS, int NST>
+struct I8Shape {
+  static constexpr int NC = 2 * TT;                 // real columns per digit block
+  static constexpr int LV = KS;                      // levels L = 0 .. KS-1 kept
+  static constexpr int TCOLS = MB * LV * NC;         // TMEM columns used
+  static_assert(TCOLS <= 512, "TMEM");
+  static constexpr int WST = KS * MB * kCore;        // W bytes per stage
+  static constexpr int BST = KS * NC * kKC;          // B bytes per stage
+  static constexpr int STAGE = WST + BST;
+  static_assert(NST >= 3, "pipeline (gather keeps 2 stages of cp.async in flight)");
+};
+
+// dynamic smem: [NST W stages][NST B stages][src table fkeys*TT int32][keys fkeys int32][bars]
+template <int MB, int TT, int KS, int NST>
+__global__ void __launch_bounds__(kI8Threads, 1)
+    k_m2l_i8(const int32_t* __restrict__ item_tile, const int32_t* __restrict__ item_seq,
+             const int64_t* __restrict__ item_k0, const int64_t* __restrict__ item_k1,
+             const int32_t* __restrict__ tile_nitem, const int32_t* __restrict__ tile_tslot,
+             const int32_t* __restrict__ tile_level, const int32_t* __restrict__ tile_keys,
+             const int32_t* __restrict__ tile_src, const uint8_t* __restrict__ tile_cols,
+             const uint8_t* __restrict__ tile_cnt, const int8_t* __restrict__ Wq, const int8_t* __restrict__ Mq,
+             const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
+             double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
+             int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys) {
+  using S = I8Shape<MB, TT, KS, NST>;
+  constexpr int NC = S::NC;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* wst = smem;
+  uint8_t* bst = smem + NST * S::WST;
+  int32_t* srcf = reinterpret_cast<int32_t*>(bst + NST * S::BST);
+  int32_t* keys = srcf + fkeys * TT;
+  uint64_t* full = reinterpret_cast<uint64_t*>(keys + ((fkeys + 1) & ~1));  // W landed (tx bytes)
+  uint64_t* fullb = full + NST;    // B gathered (kGather arrivals)
+  uint64_t* empty = fullb + NST;   // MMAs of the stage done (tcgen05.commit)
+  uint64_t* done = empty + NST;    // all MMAs of the item done
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(done + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int item = item0 + (int)blockIdx.x;
+  const int64_t k0 = item_k0[item], k1 = item_k1[item];
+  const int nk = (int)(k1 - k0);
+  const int kp = 2 * nkq, nch = kp / kKC;
+  const int tile = item_tile[item];
+
+  // per-item metadata: uncompacted source slot of every (key, target column)
+  for (int i = tid; i < nk * TT; i += kI8Threads) srcf[i] = -1;
+  for (int i = tid; i < nk; i += kI8Threads) keys[i] = tile_keys[k0 + i];
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(fullb + s, kGather);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * TT; i += kI8Threads) {
+    const int64_t kk = k0 + i / TT;
+    const int j = i % TT;
+    if (j < tile_cnt[kk]) srcf[(i / TT) * TT + tile_cols[kk * TT + j]] = tile_src[kk * TT + j];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tbase_s;
+
+  // warp roles: warp 0 lane 0 streams W (cp.async.bulk), warp 1 lane 0 issues
+  // the MMAs, warps 2-3 gather the moment digits (cp.async); NST stages in a ring
+  const int Q = nk * nch;
+  if (warp == 0) {
+    // the whole warp walks the ring (no divergent spinning lanes); lane 0 issues
+    int kq = 0, ch = 0;
+    for (int q = 0; q < Q; ++q) {
+      const int s = q % NST;
+      if (q >= NST) mbar_wait(empty + s, (uint32_t)((q / NST - 1) & 1));
+      if (lane == 0) {
+        mbar_expect_tx(full + s, S::WST);
+        bulk_g2s(wst + s * S::WST, Wq + ((int64_t)keys[kq] * nch + ch) * S::WST, S::WST, full + s);
+      }
+      __syncwarp();
+      if (++ch == nch) {
+        ch = 0;
+        ++kq;
+      }
+    }
+  } else if (warp == 1) {
+    for (int q = 0; q < Q; ++q) {
+      const int s = q % NST;
+      const uint32_t ph = (uint32_t)((q / NST) & 1);
+      mbar_wait(full + s, ph);
+      mbar_wait(fullb + s, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+        const uint32_t wa = smem_u32(wst + s * S::WST), ba = smem_u32(bst + s * S::BST);
+#pragma unroll
+        for (int i = 0; i < KS; ++i) {
+          const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
+#pragma unroll
+          for (int b = 0; b < MB; ++b) {
+            const uint64_t da = sdesc(wa + (i * MB + b) * kCore);
+#pragma unroll
+            for (int p0 = 0; p0 < ncol; p0 += 256) {
+              const int np = ncol - p0 < 256 ? ncol - p0 : 256;
+              const uint64_t db = sdesc(ba + p0 * kKC);  // 256 rows = 32 row groups x 256 B
+              mma_i8(tmem + b * S::LV * NC + i * NC + p0, da, db, idesc_i8(np), (q > 0 || i > 0) ? 1u : 0u);
+            }
+          }
+        }
+        mma_commit(empty + s);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) mma_commit(done);
+    __syncwarp();
+  } else {
+    // gather: G groups of cp.async in flight per thread; a stage's arrival on
+    // fullb follows its own wait_group + proxy fence
+    constexpr int G = 2;
+    int kq = 0, ch = 0;
+    auto arrive = [&](int qa) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
+    };
+    for (int q = 0; q < Q; ++q) {
+      const int s = q % NST;
+      if (q >= NST) mbar_wait(empty + s, (uint32_t)((q / NST - 1) & 1));
+      uint8_t* bb = bst + s * S::BST;
+      const int32_t* sf = srcf + kq * TT;
+      // lane = (column of a group of 4, piece 0..7 of a round): every warp
+      // instruction reads 4 contiguous 128-byte runs and writes 4 wavefronts
+      const int cl = lane >> 3, p8 = lane & 7;
+#pragma unroll 1
+      for (int cg = warp - 2; cg < TT / 4; cg += 2) {
+        const int c = 4 * cg + cl;
+        const int src = sf[c];
+        const int8_t* g = Mq + ((int64_t)src * nch + ch) * (KS * 64);
+#pragma unroll
+        for (int r = 0; r < (KS * 4 + 7) / 8; ++r) {
+          const int pc = 8 * r + p8;  // piece: digit j, kb, h
+          if (pc < KS * 4) {
+            const int h = pc & 1, kb = (pc >> 1) & 1, j = pc >> 2;
+            const int n = j * NC + 2 * c + h;
+            uint8_t* dst = bb + ((n >> 3) * 2 + kb) * 128 + (n & 7) * 16;
+            if (src >= 0) cp_async16(dst, g + pc * 16);
+            else *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
+          }
+        }
+      }
+      cp_async_commit();
+      if (q >= G) {
+        cp_async_wait<G>();
+        arrive(q - G);
+      }
+      if (++ch == nch) {
+        ch = 0;
+        ++kq;
+      }
+    }
+    cp_async_wait<0>();
+    for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qa);
+  }
+  // all MMAs of the item done
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // ---- epilogue: levels -> FP64, chained accumulation into the tile
+  const int seq = item_seq[item], nit = tile_nitem[tile];
+  const int lvl = tile_level[tile];
+  const int exs = level_exp(lvmax_w, lvl) + level_exp(lvmax_v, lvl) + 2;
+  if (seq > 0) {
+    if (tid == 0) {
+      long long spins = 0;
+      while (ld_acquire(ticket + tile) != seq) {
+        __nanosleep(200);
+        if (++spins > (1ll << 26)) {  // > ~10 s: report instead of hanging
+          atomicOr(err, 2);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const bool last = seq == nit - 1;
+  double fL[S::LV];  // level weights 2^(-7(L+2)) S_W S_V
+#pragma unroll
+  for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, exs - 7 * (L + 2));
+  double* A = tile_acc + (int64_t)tile * n_pad * NC;
+#pragma unroll 1
+  for (int b = 0; b < MB; ++b) {
+    const int row = b * 128 + warp * 32 + lane;
+#pragma unroll 1
+    for (int g = 0; g < NC / 8; ++g) {
+      uint32_t r[S::LV][8];
+#pragma unroll
+      for (int L = 0; L < S::LV; ++L)
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + b * S::LV * NC + L * NC + 8 * g, r[L]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row >= n_pad) continue;
+      double v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        double a = 0.0;
+#pragma unroll
+        for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
+        v[e] = a;
+      }
+      double* pa = A + (int64_t)row * NC + 8 * g;
+      if (seq > 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += __ldcg(pa + e);
+      }
+      if (last) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int col = 8 * g + e;
+          const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
+          if (ts >= 0) loc[(int64_t)ts * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) __stcg(pa + e, v[e]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (!last) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(ticket + tile, seq + 1);
+  }
+}
+
+template <int MB, int TT, int NST>
+size_t i8_smem(int fkeys) {
+  using S = I8Shape<MB, TT, kI8Digits, NST>;
+  return (size_t)NST * S::STAGE + (size_t)fkeys * TT * 4 + (size_t)((fkeys + 1) & ~1) * 4 + (3 * NST + 1) * 8 + 16;
+}
+
+template <int MB, int TT, int NST>
+void run_i8(cudaStream_t st, const M2LI8Args& a) {
+  auto kern = k_m2l_i8<MB, TT, kI8Digits, NST>;
+  const size_t sm = i8_smem<MB, TT, NST>(a.fkeys);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  kern<<<a.n_item, kI8Threads, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
+                                         a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
+                                         a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.err, a.item0, a.nkq,
+                                         a.n_pad, a.fkeys);
+}
+
+}  // namespace
+
+int m2l_i8_supported(int n, int tile) {
+  const int mb = (n + 127) / 128;
+  return (mb == 1 && tile == 32) || (mb == 2 && tile == 16);
+}
+int m2l_i8_fkeys(int nkq) {
+  // |digit| <= 64: one key adds at most KS * KP * 64^2 to a level accumulator
+  const int64_t per_key = (int64_t)kI8Digits * 2 * nkq * 4096;
+  const int64_t f = (int64_t)0x7fffffff / per_key;
+  return (int)std::min<int64_t>(256, f);
+}
+int64_t m2l_i8_wbytes_per_key(int n, int nkq) { return (int64_t)kI8Digits * ((n + 127) / 128) * kCore * (2 * nkq / kKC); }
+int64_t m2l_i8_mbytes_per_slot(int nkq) { return (int64_t)kI8Digits * 2 * 2 * nkq; }
+
+void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
+                        const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq) {
+  if (nkeys <= 0) return;
+  dim3 grid((unsigned)nkeys, (unsigned)((n + kCplRows - 1) / kCplRows));
+  k_coupling_i8<kI8Digits><<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
+                                                 (n + 127) / 128);
+}
+void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
+                      int nkq, unsigned long long* lvmax_v, int8_t* Mq) {
+  if (nslots <= 0) return;
+  cudaMemsetAsync(lvmax_v, 0, sizeof(unsigned long long) * kMaxLevels, st);
+  k_mom_max<<<(unsigned)nslots, 128, 0, st>>>(mom, slot_level, n, n_pad, lvmax_v);
+  k_mom_quant<kI8Digits><<<(unsigned)nslots, 128, 0, st>>>(mom, slot_level, lvmax_v, n, n_pad, nkq, Mq);
+}
+int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
+  if (a.n_item <= 0) return 0;
+  const int mb = (n + 127) / 128;
+  if (mb == 1 && tile == 32) run_i8<1, 32, 4>(st, a);
+  else if (mb == 2 && tile == 16) run_i8<2, 16, 3>(st, a);
+  else return 1;
+  return 0;
+}
+
+}  // namespace fdhelm

@@ -54,4 +54,35 @@ struct M2LArgs {
 // returns 0 on success, nonzero if the n_pad / tile combination is not compiled
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a);
 
+// ---- k_m2l_i8.cu: M2L on tcgen05 int8 tensor cores (exact fixed-point digit products)
+#ifndef FDH_I8_DIGITS
+#define FDH_I8_DIGITS 7
+#endif
+constexpr int kI8Digits = FDH_I8_DIGITS;  // base-128 digits per FP64 value (7 x 7 = 49 bits)
+struct M2LI8Args {
+  int n_item = 0, item0 = 0;
+  const int32_t *item_tile = nullptr, *item_seq = nullptr;
+  const int64_t *item_k0 = nullptr, *item_k1 = nullptr;
+  const int32_t *tile_nitem = nullptr, *tile_tslot = nullptr, *tile_level = nullptr, *tile_keys = nullptr,
+                *tile_src = nullptr;
+  const uint8_t *tile_cols = nullptr, *tile_cnt = nullptr;
+  const int8_t *Wq = nullptr, *Mq = nullptr;
+  const unsigned long long *lvmax_w = nullptr, *lvmax_v = nullptr;
+  double* tile_acc = nullptr;
+  int* ticket = nullptr;
+  double* loc = nullptr;
+  int* err = nullptr;
+  int nkq = 0, n_pad = 0, fkeys = 0;
+};
+int m2l_i8_supported(int n, int tile);
+int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
+int64_t m2l_i8_wbytes_per_key(int n, int nkq);
+int64_t m2l_i8_mbytes_per_slot(int nkq);
+void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
+                        const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq);
+void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
+                      int nkq, unsigned long long* lvmax_v, int8_t* Mq);
+int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a);
+
 }  // namespace fdhelm

@@ -673,13 +673,14 @@ void build_m2l(Plan& P) {
   const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
   P.m2l_chunk = cw;
   std::vector<std::array<int64_t, 4>> items;  // chunk, tile, k0, k1
+  const int64_t fk = P.prm.m2l_fkeys > 0 ? P.prm.m2l_fkeys : INT64_MAX;  // k_m2l_i8: exact int32 sums
   for (int64_t tl = 0; tl < ntile; ++tl) {
     int64_t j = P.tile_kptr[tl];
     const int64_t e = P.tile_kptr[tl + 1];
     while (j < e) {
       const int64_t c = P.tile_keys[j] / cw;
       int64_t k = j;
-      while (k < e && P.tile_keys[k] / cw == c) ++k;
+      while (k < e && P.tile_keys[k] / cw == c && k - j < fk) ++k;
       items.push_back({c, tl, j, k});
       j = k;
     }

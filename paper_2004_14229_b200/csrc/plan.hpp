@@ -36,6 +36,8 @@ struct PlanParams {
   int depth_cap = 30;
   int zero_diagonal = 0;
   int tile = 16;       // M2L target slots per tile
+  int m2l_impl = 0;    // 0: FP64 DMMA (k_m2l_gemm), 1: int8 tcgen05 digits (k_m2l_i8)
+  int m2l_fkeys = 0;   // > 0: at most this many keys per M2L work item
   int rank = 0, world = 1;
   bool gpu_structure = false;  // trees / partition / directions on the device (k_setup.cu)
 };
