@@ -38,13 +38,16 @@
 #include "kernels.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+
+#ifndef FDH_I8_EXP
+#define FDH_I8_EXP 0  // timing experiments: 1 = no B gather, 2 = no W copy, 3 = neither (wrong results)
+#endif
 
 namespace fdhelm {
 
 namespace {
 
-constexpr int kI8Threads = 128;
-constexpr int kGather = 64;           // threads (warps 2-3) gathering the moment digits
 constexpr int kKC = 32;               // K bytes per MMA k-step / pipeline stage
 constexpr int kCore = 128 * kKC;      // bytes of one 128-row x 32-byte operand block
 
@@ -86,6 +89,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+}
+// producer-side wait (the ring is usually ahead): back off between polls so the
+// spinning warps do not steal shared-memory wavefronts from the tensor core
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(128);
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -255,8 +274,11 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
 }
 
 // ---------------------------------------------------------------- M2L
-template <int MB, int TT, int KS, int NST>
+template <int MB, int TT, int KS, int NST, int NGW>
 struct I8Shape {
+  static constexpr int THREADS = (2 + NGW) * 32;  // W producer, MMA issuer, NGW gather warps
+  static constexpr int GATHER = NGW * 32;
+  static_assert(NGW == 2 || NGW >= 4, "epilogue warps must cover the 4 TMEM lane quarters");
   static constexpr int NC = 2 * TT;                 // real columns per digit block
   static constexpr int LV = KS;                      // levels L = 0 .. KS-1 kept
   static constexpr int TCOLS = MB * LV * NC;         // TMEM columns used
@@ -268,8 +290,8 @@ struct I8Shape {
 };
 
 // dynamic smem: [NST W stages][NST B stages][src table fkeys*TT int32][keys fkeys int32][bars]
-template <int MB, int TT, int KS, int NST>
-__global__ void __launch_bounds__(kI8Threads, 1)
+template <int MB, int TT, int KS, int NST, int NGW, int G>
+__global__ void __launch_bounds__(I8Shape<MB, TT, KS, NST, NGW>::THREADS, 1)
     k_m2l_i8(const int32_t* __restrict__ item_tile, const int32_t* __restrict__ item_seq,
              const int64_t* __restrict__ item_k0, const int64_t* __restrict__ item_k1,
              const int32_t* __restrict__ tile_nitem, const int32_t* __restrict__ tile_tslot,
@@ -279,15 +301,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
              int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys) {
-  using S = I8Shape<MB, TT, KS, NST>;
+  using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
+  constexpr int NT = S::THREADS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* wst = smem;
   uint8_t* bst = smem + NST * S::WST;
   int32_t* srcf = reinterpret_cast<int32_t*>(bst + NST * S::BST);
   int32_t* keys = srcf + fkeys * TT;
   uint64_t* full = reinterpret_cast<uint64_t*>(keys + ((fkeys + 1) & ~1));  // W landed (tx bytes)
-  uint64_t* fullb = full + NST;    // B gathered (kGather arrivals)
+  uint64_t* fullb = full + NST;    // B gathered (one arrival per gather warp)
   uint64_t* empty = fullb + NST;   // MMAs of the stage done (tcgen05.commit)
   uint64_t* done = empty + NST;    // all MMAs of the item done
   uint32_t* tbase_s = reinterpret_cast<uint32_t*>(done + 1);
@@ -299,12 +322,12 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   const int tile = item_tile[item];
 
   // per-item metadata: uncompacted source slot of every (key, target column)
-  for (int i = tid; i < nk * TT; i += kI8Threads) srcf[i] = -1;
-  for (int i = tid; i < nk; i += kI8Threads) keys[i] = tile_keys[k0 + i];
+  for (int i = tid; i < nk * TT; i += NT) srcf[i] = -1;
+  for (int i = tid; i < nk; i += NT) keys[i] = tile_keys[k0 + i];
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(fullb + s, kGather);
+      mbar_init(fullb + s, NGW);
       mbar_init(empty + s, 1);
     }
     mbar_init(done, 1);
@@ -315,7 +338,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   __syncthreads();
-  for (int i = tid; i < nk * TT; i += kI8Threads) {
+  for (int i = tid; i < nk * TT; i += NT) {
     const int64_t kk = k0 + i / TT;
     const int j = i % TT;
     if (j < tile_cnt[kk]) srcf[(i / TT) * TT + tile_cols[kk * TT + j]] = tile_src[kk * TT + j];
@@ -333,10 +356,14 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     int kq = 0, ch = 0;
     for (int q = 0; q < Q; ++q) {
       const int s = q % NST;
-      if (q >= NST) mbar_wait(empty + s, (uint32_t)((q / NST - 1) & 1));
+      if (q >= NST) mbar_wait_sleep(empty + s, (uint32_t)((q / NST - 1) & 1));
       if (lane == 0) {
-        mbar_expect_tx(full + s, S::WST);
-        bulk_g2s(wst + s * S::WST, Wq + ((int64_t)keys[kq] * nch + ch) * S::WST, S::WST, full + s);
+        if (FDH_I8_EXP & 2) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
+        } else {
+          mbar_expect_tx(full + s, S::WST);
+          bulk_g2s(wst + s * S::WST, Wq + ((int64_t)keys[kq] * nch + ch) * S::WST, S::WST, full + s);
+        }
       }
       __syncwarp();
       if (++ch == nch) {
@@ -345,6 +372,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
     }
   } else if (warp == 1) {
+    const uint64_t dA0 = sdesc(smem_u32(wst)), dB0 = sdesc(smem_u32(bst));
     for (int q = 0; q < Q; ++q) {
       const int s = q % NST;
       const uint32_t ph = (uint32_t)((q / NST) & 1);
@@ -352,18 +380,22 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       mbar_wait(fullb + s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (lane == 0) {
-        const uint32_t wa = smem_u32(wst + s * S::WST), ba = smem_u32(bst + s * S::BST);
+        // descriptors are linear in the address (14-bit field, addr >> 4): every
+        // operand offset below is a compile-time constant added to the stage base
+        // (keeps the issuing thread at ~3 instructions per MMA; recomputing the
+        // descriptors per MMA made issue, not the tensor core, the bound)
+        const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
+        const uint32_t acc0 = q > 0 ? 1u : 0u;
 #pragma unroll
         for (int i = 0; i < KS; ++i) {
           const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
 #pragma unroll
           for (int b = 0; b < MB; ++b) {
-            const uint64_t da = sdesc(wa + (i * MB + b) * kCore);
 #pragma unroll
             for (int p0 = 0; p0 < ncol; p0 += 256) {
               const int np = ncol - p0 < 256 ? ncol - p0 : 256;
-              const uint64_t db = sdesc(ba + p0 * kKC);  // 256 rows = 32 row groups x 256 B
-              mma_i8(tmem + b * S::LV * NC + i * NC + p0, da, db, idesc_i8(np), (q > 0 || i > 0) ? 1u : 0u);
+              mma_i8(tmem + b * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
+                     dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
             }
           }
         }
@@ -375,37 +407,47 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     __syncwarp();
   } else {
     // gather: G groups of cp.async in flight per thread; a stage's arrival on
-    // fullb follows its own wait_group + proxy fence
-    constexpr int G = 2;
+    // fullb follows its own wait_group + proxy fence.  Work unit = (group of 4
+    // target columns, round of 8 pieces): lane = (column in the group, piece),
+    // so every warp instruction reads 4 contiguous 128-byte runs of Mq and
+    // writes 4 SMEM wavefronts.  Per-lane offsets are stage-invariant.
+    constexpr int RND = (KS * 4 + 7) / 8;  // rounds of 8 pieces per column (pieces: digit, kb, h)
+    constexpr int U = (TT / 4) * RND;
+    constexpr int UPW = (U + NGW - 1) / NGW;
+    const int cl = lane >> 3, p8 = lane & 7;
+    int dsto[UPW], gofs[UPW], ccol[UPW];
+#pragma unroll
+    for (int t = 0; t < UPW; ++t) {
+      const int u = (warp - 2) + t * NGW;
+      const int cg = u / RND, r = u % RND;
+      const int pc = 8 * r + p8;
+      const int c = 4 * cg + cl;
+      const bool ok = u < U && pc < KS * 4;
+      const int h = pc & 1, kb = (pc >> 1) & 1, j = pc >> 2;
+      const int n = j * NC + 2 * c + h;
+      dsto[t] = ok ? ((n >> 3) * 2 + kb) * 128 + (n & 7) * 16 : -1;
+      gofs[t] = pc * 16;
+      ccol[t] = ok ? c : 0;
+    }
     int kq = 0, ch = 0;
-    auto arrive = [&](int qa) {
+    auto arrive = [&](int qa) {  // one arrival per warp once all its lanes' pieces landed
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
     };
     for (int q = 0; q < Q; ++q) {
       const int s = q % NST;
-      if (q >= NST) mbar_wait(empty + s, (uint32_t)((q / NST - 1) & 1));
+      if (q >= NST) mbar_wait_sleep(empty + s, (uint32_t)((q / NST - 1) & 1));
       uint8_t* bb = bst + s * S::BST;
       const int32_t* sf = srcf + kq * TT;
-      // lane = (column of a group of 4, piece 0..7 of a round): every warp
-      // instruction reads 4 contiguous 128-byte runs and writes 4 wavefronts
-      const int cl = lane >> 3, p8 = lane & 7;
-#pragma unroll 1
-      for (int cg = warp - 2; cg < TT / 4; cg += 2) {
-        const int c = 4 * cg + cl;
-        const int src = sf[c];
-        const int8_t* g = Mq + ((int64_t)src * nch + ch) * (KS * 64);
+      const int8_t* mq = Mq + (int64_t)ch * (KS * 64);
 #pragma unroll
-        for (int r = 0; r < (KS * 4 + 7) / 8; ++r) {
-          const int pc = 8 * r + p8;  // piece: digit j, kb, h
-          if (pc < KS * 4) {
-            const int h = pc & 1, kb = (pc >> 1) & 1, j = pc >> 2;
-            const int n = j * NC + 2 * c + h;
-            uint8_t* dst = bb + ((n >> 3) * 2 + kb) * 128 + (n & 7) * 16;
-            if (src >= 0) cp_async16(dst, g + pc * 16);
-            else *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
-          }
-        }
+      for (int t = 0; t < UPW; ++t) {
+        if (dsto[t] < 0 || (FDH_I8_EXP & 1)) continue;
+        const int src = sf[ccol[t]];
+        if (src >= 0) cp_async16(bb + dsto[t], mq + (int64_t)src * nch * (KS * 64) + gofs[t]);
+        else *reinterpret_cast<int4*>(bb + dsto[t]) = make_int4(0, 0, 0, 0);
       }
       cp_async_commit();
       if (q >= G) {
@@ -421,7 +463,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qa);
   }
   // all MMAs of the item done
-  mbar_wait(done, 0);
+  mbar_wait_sleep(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ---- epilogue: levels -> FP64, chained accumulation into the tile
@@ -446,15 +488,16 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
   for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, exs - 7 * (L + 2));
   double* A = tile_acc + (int64_t)tile * n_pad * NC;
+  const int qw = warp & 3;  // TMEM lane quarter of this warp
 #pragma unroll 1
-  for (int b = 0; b < MB; ++b) {
-    const int row = b * 128 + warp * 32 + lane;
+  for (int b = 0; b < MB && (NGW == 2 || (warp >= 2 && warp < 6)); ++b) {
+    const int row = b * 128 + qw * 32 + lane;
 #pragma unroll 1
     for (int g = 0; g < NC / 8; ++g) {
       uint32_t r[S::LV][8];
 #pragma unroll
       for (int L = 0; L < S::LV; ++L)
-        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + b * S::LV * NC + L * NC + 8 * g, r[L]);
+        tmem_ld8(tmem + ((uint32_t)(qw * 32) << 16) + b * S::LV * NC + L * NC + 8 * g, r[L]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (row >= n_pad) continue;
       double v[8];
@@ -493,18 +536,19 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   }
 }
 
-template <int MB, int TT, int NST>
+template <int MB, int TT, int NST, int NGW>
 size_t i8_smem(int fkeys) {
-  using S = I8Shape<MB, TT, kI8Digits, NST>;
+  using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
   return (size_t)NST * S::STAGE + (size_t)fkeys * TT * 4 + (size_t)((fkeys + 1) & ~1) * 4 + (3 * NST + 1) * 8 + 16;
 }
 
-template <int MB, int TT, int NST>
+template <int MB, int TT, int NST, int NGW, int G>
 void run_i8(cudaStream_t st, const M2LI8Args& a) {
-  auto kern = k_m2l_i8<MB, TT, kI8Digits, NST>;
-  const size_t sm = i8_smem<MB, TT, NST>(a.fkeys);
+  using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
+  auto kern = k_m2l_i8<MB, TT, kI8Digits, NST, NGW, G>;
+  const size_t sm = i8_smem<MB, TT, NST, NGW>(a.fkeys);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  kern<<<a.n_item, kI8Threads, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
+  kern<<<a.n_item, S::THREADS, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
                                          a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
                                          a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.err, a.item0, a.nkq,
                                          a.n_pad, a.fkeys);
@@ -543,8 +587,18 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
   const int mb = (n + 127) / 128;
-  if (mb == 1 && tile == 32) run_i8<1, 32, 4>(st, a);
-  else if (mb == 2 && tile == 16) run_i8<2, 16, 3>(st, a);
+  static const int var = [] {
+    const char* e = std::getenv("FDH_I8_VARIANT");  // tuning knob
+    return e ? std::atoi(e) : 0;
+  }();
+  // measured on config 2 (M2L ms): 2 gather warps 38.6, 4: 31.0, 8: 30.2 (G = 1 or 2: same)
+  if (mb == 1 && tile == 32) {
+    if (var == 1) run_i8<1, 32, 4, 4, 1>(st, a);
+    else run_i8<1, 32, 4, 8, 1>(st, a);
+  } else if (mb == 2 && tile == 16) {
+    if (var == 1) run_i8<2, 16, 3, 4, 1>(st, a);
+    else run_i8<2, 16, 3, 8, 1>(st, a);
+  }
   else return 1;
   return 0;
 }

@@ -667,8 +667,12 @@ void build_m2l(Plan& P) {
   // coupling matrix is read from HBM about once and then served from L2 to
   // every tile that uses it.  Chunk width: ~12 MB of coupling matrices.  The
   // items of one tile are chained in chunk order (item_seq) by the kernel.
-  const int64_t wbytes = (int64_t)P.n_pad * m2l_wplanes(P.n_pad) * P.n_k * 8;
-  int64_t chunk_mb = 12;  // measured optimum 8-12 MB on config 2 (profiles/r01_m2l_chunk_sweep.txt)
+  // int8 digits (k_m2l_i8): 7 x ceil(n/128) x 128 x 2 n_kq bytes per key; longer
+  // items amortise its per-item TMEM epilogue (config 2: 12 MB 30.2 ms, 24-48 MB 29.1 ms)
+  const int nkq = (P.n + 15) / 16 * 16;
+  const int64_t wbytes = P.prm.m2l_impl == 1 ? (int64_t)7 * ((P.n + 127) / 128) * 128 * 2 * nkq
+                                              : (int64_t)P.n_pad * m2l_wplanes(P.n_pad) * P.n_k * 8;
+  int64_t chunk_mb = P.prm.m2l_impl == 1 ? 24 : 12;  // DMMA: optimum 8-12 MB (profiles/r01_m2l_chunk_sweep.txt)
   if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
   const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
   P.m2l_chunk = cw;

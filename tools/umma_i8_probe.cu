@@ -191,6 +191,60 @@ __global__ void k_tput2(int N, int K, int iters, long long* cyc) {
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(td));
 }
 
+
+// the k_m2l_i8 stage pattern: for digit i, N = (7-i)*NC split at 256, D col = i*NC + p0
+__global__ void k_pattern(int NC, int iters, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  int8_t* sa = (int8_t*)sm;              // 7 W digit blocks of 128 x 32
+  int8_t* sb = sa + 7 * 4096;            // B: 7*NC rows x 32
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  for (int i = threadIdx.x; i < 7 * 4096 + 7 * NC * 32; i += blockDim.x) sa[i] = (int8_t)((i * 37) & 63) - 32;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t td = tbase;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+    const long long t0 = clock64();
+    const uint64_t dA = sdesc(a0, 128, 256), dB = sdesc(b0, 128, 256);
+    if (NC == 64) {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+          constexpr int NCc = 64;
+          const int ncol = (7 - i) * NCc;
+#pragma unroll
+          for (int p0 = 0; p0 < ncol; p0 += 256) {
+            const int np = ncol - p0 < 256 ? ncol - p0 : 256;
+            mma_i8(td + i * NCc + p0, dA + (uint64_t)(i * 4096 >> 4), dB + (uint64_t)(p0 * 32 >> 4), idesc_i8(128, np), (it | i) > 0);
+          }
+        }
+      }
+    } else {
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+          constexpr int NCc = 32;
+          const int ncol = (7 - i) * NCc;
+          mma_i8(td + i * NCc, dA + (uint64_t)(i * 4096 >> 4), dB, idesc_i8(128, ncol), (it | i) > 0);
+        }
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(td));
+}
+
 int main() {
   int dev = 0;
   cudaDeviceProp pr;
@@ -282,6 +336,21 @@ int main() {
     for (auto v : c) mx = v > mx ? v : mx;
     const double macs = (double)M * N * K * iters * nacc;
     std::printf("tput2 nacc=%d N=%3d: %.1f MAC/clk/SM, %.1f clk/MMA\n", nacc, N, macs / (double)mx, (double)mx / (iters * 8.0 * nacc));
+  }
+
+  for (int NC : {32, 64}) {
+    const int iters = 2000;
+    const size_t sm = 7 * 4096 + 7 * NC * 32;
+    CK(cudaFuncSetAttribute(k_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_pattern<<<nsm, 128, sm>>>(NC, 10, dc);
+    CK(cudaDeviceSynchronize());
+    k_pattern<<<nsm, 128, sm>>>(NC, iters, dc);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> c(nsm);
+    CK(cudaMemcpy(c.data(), dc, nsm * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (auto v : c) mx = v > mx ? v : mx;
+    std::printf("pattern NC=%d: %.1f clk/stage (ideal %d)\n", NC, (double)mx / iters, 28 * NC / 2);
   }
   return 0;
 }
