@@ -130,6 +130,49 @@ def cpu_oracle_sample(c, tg, sr, q, target_s=12.0, o=None, seed=7):
     }
 
 
+def roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traffic):
+    """Roofline of the M2L kernel: the int8 tcgen05 digit GEMM (k_m2l_i8) against
+    the measured int8 tensor peak, or the FP64 DMMA GEMM against the FP64 peak."""
+    share = gemm_ms / ms_per_step if ms_per_step else None
+    fp64 = {"achieved_tflops": achieved, "fp64_peak_tflops": peak,
+            "ratio": (achieved / peak) if (achieved and peak) else None,
+            "note": "algorithmic FP64 flop (8 n^2 per admissible block) per second of the M2L kernel, against the "
+                    "measured FP64 DMMA peak"}
+    if st["m2l_impl"] == 1:
+        tops = F.tensor_peak_tops(0)
+        # algorithmic int8 work: the 28 digit-pair products (i + j <= 6 of 7 digits) of every
+        # real MAC of the complex product (4 n^2 per block, 2 ops per MAC)
+        alg = 28.0 * m2l_flops
+        ach = alg / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        iss = st["m2l_i8_ops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        return {"bound": "tensor", "kernel": "k_m2l_i8 (tcgen05.mma kind::i8, exact 7-digit fixed-point products, "
+                                            "TMEM int32 level accumulators)",
+                "achieved": ach, "peak": tops, "unit": "TOPS", "frac": (ach / tops) if (ach and tops) else None,
+                "traffic": traffic,
+                "peak_source": "measured live: fdh_tensor_peak_tops(0) int8 tcgen05 microbenchmark, M=128 N=256 "
+                               "(MEASURED_PEAKS.json has no int8 entry; its bf16 burst 1625.8 TF/s x 2 = 3252 for "
+                               "comparison)",
+                "algorithmic": f"28 digit products x 8 n^2 ops per admissible block x N_C={st['n_c']} = {alg:.4g} "
+                               f"int8 ops per launch",
+                "issued_ops": st["m2l_i8_ops"], "issued_frac": (iss / tops) if (iss and tops) else None,
+                "issued_note": "int8 ops the kernel issues: every target column of a tile for every key of the tile "
+                               "(absent columns are zero), rows padded to 128, K to 2 x 16k",
+                "fp64_equivalent": fp64, "gemm_ms": gemm_ms, "share_of_step": share}
+    return {"bound": "tensor", "kernel": "k_m2l_gemm (FP64 DMMA mma.sync.m8n8k4)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+            "peak_source": "measured live: fdh_fp64_peak_tflops(0) DMMA microbenchmark (no FP64 entry in "
+                           "MEASURED_PEAKS.json)",
+            "algorithmic": f"8 n^2 flop per admissible block x N_C={st['n_c']} = {m2l_flops:.4g} flop per "
+                           f"launch (SURVEY.md 8(d); the count holds for a 3M complex product)",
+            "issued_flop": st["m2l_flops_executed"],
+            "issued_frac": (st["m2l_flops_executed"] / (gemm_ms * 1e-3) / 1e12 / peak
+                            if (gemm_ms > 0 and peak) else None),
+            "issued_note": "flop the kernel issues on DMMA: Gauss 3-multiplication product (6 n^2) for "
+                           "8-target n-tiles, 8 n^2 real GEMM for <= 4, incl. padding columns",
+            "gemm_ms": gemm_ms, "share_of_step": share}
+
+
 def run_reference(args, c, rank, world):
     """--impl reference: the reference algorithm on the host cores (oracle port)."""
     if rank != 0:
@@ -256,7 +299,7 @@ def run_ours(args, c, rank, world, local_rank):
 
     if rank != 0:
         return
-    # ---- roofline of the dominant kernel (M2L GEMM on FP64 DMMA)
+    # ---- roofline of the dominant kernel (the M2L GEMM)
     peak = F.fp64_peak_tflops(0)
     n = (c.m + 1) ** 3
     m2l_flops = 8.0 * n * n * st["n_c"]  # algorithmic
@@ -266,7 +309,7 @@ def run_ours(args, c, rank, world, local_rank):
     if os.path.exists(PROFILE_TRAFFIC):
         try:
             tr = json.load(open(PROFILE_TRAFFIC))
-            traffic = tr.get(f"cfg{c.cfg}")
+            traffic = tr.get(f"cfg{c.cfg}{'_i8' if st['m2l_impl'] == 1 else ''}")
         except Exception:
             traffic = None
     ph = st["phase_ms"]
@@ -274,24 +317,14 @@ def run_ours(args, c, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "complex128 (f64)",
+        "vs_baseline": None,
+        "dtype": ("complex128 (f64; M2L as exact int8 x int8 -> int32 digit products of 49-bit fixed-point operands "
+                  "on tcgen05)" if st["m2l_impl"] == 1 else "complex128 (f64)"),
         "data": "synthetic (seeded uniform / Gaussian-mixture points, U(-1,1) complex charges; SURVEY.md 8(d))",
         "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": f"target-leaf shards x{world}",
                    "l2": "flushed between timed steps (256 MB write, outside the step events)",
                    "setup_s": setup_s},
-        "roofline": {"bound": "tensor", "kernel": "k_m2l_gemm (FP64 DMMA mma.sync.m8n8k4)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                     "peak_source": "measured live: fdh_fp64_peak_tflops(0) DMMA microbenchmark (no FP64 entry in "
-                                    "MEASURED_PEAKS.json)",
-                     "algorithmic": f"8 n^2 flop per admissible block x N_C={st['n_c']} = {m2l_flops:.4g} flop per "
-                                    f"launch (SURVEY.md 8(d); the count holds for a 3M complex product)",
-                     "issued_flop": st["m2l_flops_executed"],
-                     "issued_frac": (st["m2l_flops_executed"] / (gemm_ms * 1e-3) / 1e12 / peak
-                                     if (gemm_ms > 0 and peak) else None),
-                     "issued_note": "flop the kernel issues on DMMA: Gauss 3-multiplication product (6 n^2) for "
-                                    "8-target n-tiles, 8 n^2 real GEMM for <= 4, incl. padding columns",
-                     "gemm_ms": gemm_ms, "share_of_step": gemm_ms / ms_per_step if ms_per_step else None},
+        "roofline": roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traffic),
         "phases_ms": ph,
         "p2p": {"pairs": st["m_d"], "ms": p2p_ms,
                 "tflops_24flop_per_pair": 24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else None},

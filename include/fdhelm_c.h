@@ -156,6 +156,10 @@ const char* fdh_version(void);
 /* Measured FP64 peak of the current device in TFLOP/s (kind 0: DMMA
  * mma.sync.m8n8k4.f64, 1: DFMA), the roofline denominator of M2L / P2P. */
 double fdh_fp64_peak_tflops(int kind);
+/* Measured dense tensor peak of the current device in TOPS (kind 0: int8
+ * tcgen05.mma kind::i8, M=128 N=256 from shared memory), the roofline
+ * denominator of the int8 M2L kernel (k_m2l_i8). */
+double fdh_tensor_peak_tops(int kind);
 
 #ifdef __cplusplus
 }

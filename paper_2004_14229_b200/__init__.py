@@ -29,7 +29,7 @@ PHASES = ["h2d", "s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "d2h"]
 SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_plan_only", "fdh_apply", "fdh_apply_device", "fdh_stream",
            "fdh_set_timing", "fdh_get_stats", "fdh_export_tree", "fdh_export_perm", "fdh_export_lplus",
            "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_structure_digest", "fdh_destroy", "fdh_last_error", "fdh_version",
-           "fdh_fp64_peak_tflops"]
+           "fdh_fp64_peak_tflops", "fdh_tensor_peak_tops"]
 
 
 class FdhStats(C.Structure):
@@ -92,6 +92,8 @@ def lib():
         L.fdh_structure_digest.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.fdh_fp64_peak_tflops.argtypes = [C.c_int]
         L.fdh_fp64_peak_tflops.restype = C.c_double
+        L.fdh_tensor_peak_tops.argtypes = [C.c_int]
+        L.fdh_tensor_peak_tops.restype = C.c_double
         _lib = L
     return _lib
 
@@ -214,3 +216,8 @@ def version() -> str:
 def fp64_peak_tflops(kind: int = 0) -> float:
     """Measured FP64 peak on the current device (0: DMMA m8n8k4, 1: DFMA)."""
     return float(lib().fdh_fp64_peak_tflops(kind))
+
+
+def tensor_peak_tops(kind: int = 0) -> float:
+    """Measured int8 tcgen05 dense peak (TOPS) of the current device."""
+    return float(lib().fdh_tensor_peak_tops(kind))

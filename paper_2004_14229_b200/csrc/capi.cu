@@ -585,11 +585,16 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     // nodes per box, i.e. m <= 5), FP64 DMMA otherwise; FDH_M2L_IMPL=dmma|i8 overrides
     const int nbox = (m + 1) * (m + 1) * (m + 1);
     const char* mi = std::getenv("FDH_M2L_IMPL");
-    const bool want_i8 = device && m >= 1 && nbox <= 256 && !(mi && std::string(mi) == "dmma");
+    const char* pi = std::getenv("FDH_PLAN_I8");  // analysis knob: plan-only operators with the int8 plan
+    const char* otf = std::getenv("FDH_W_ONTHEFLY");  // per-apply coupling generation: FP64 DMMA path only
+    const bool want_i8 = (device || (pi && pi[0] == '1')) && m >= 1 && nbox <= 256 &&
+                         !(mi && std::string(mi) == "dmma") && !(otf && otf[0] == '1');
     if (want_i8) {
       prm.m2l_impl = 1;
       prm.tile = nbox <= 128 ? 32 : 16;
       prm.m2l_fkeys = m2l_i8_fkeys((nbox + 15) / 16 * 16);
+      if (const char* fk = std::getenv("FDH_M2L_FKEYS"))  // testing knob: shorter items (more chaining)
+        prm.m2l_fkeys = std::max(1, std::min(prm.m2l_fkeys, std::atoi(fk)));
     }
     build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
     if (device) {
@@ -730,12 +735,13 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->w_segments = (int64_t)o->segs.size();
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
-  s->m2l_impl = o->i8 ? 1 : 0;
-  if (o->i8) {
+  s->m2l_impl = P.prm.m2l_impl;
+  if (P.prm.m2l_impl == 1) {
     // int8 MACs issued by k_m2l_i8: per (tile, key) and K byte: 128 rows x sum_i (KS - i) 2 TT columns per m-block
     const int64_t cols = (int64_t)kI8Digits * (kI8Digits + 1) / 2 * 2 * P.prm.tile;
+    const int64_t nkq = (P.n + 15) / 16 * 16;
     s->m2l_flops_executed = 0;
-    s->m2l_i8_ops = 2 * (int64_t)P.tile_keys.size() * ((P.n + 127) / 128) * 128 * (2 * (int64_t)o->nkq) * cols;
+    s->m2l_i8_ops = 2 * (int64_t)P.tile_keys.size() * ((P.n + 127) / 128) * 128 * (2 * nkq) * cols;
   }
   return FDH_OK;
 }

@@ -1,6 +1,8 @@
-// k_peak.cu -- FP64 peak microbenchmarks (the roofline denominator for the
-// FP64-bound phases; MEASURED_PEAKS.json carries no FP64 figure).
+// k_peak.cu -- peak microbenchmarks for the roofline denominators that
+// MEASURED_PEAKS.json does not carry: FP64 (DMMA / DFMA) and the int8 tcgen05
+// tensor core (k_m2l_i8).
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 #include "../../include/fdhelm_c.h"
 
@@ -35,7 +37,79 @@ __global__ void k_peak_dfma(double* out, int iters, double a, double b) {
   for (int i = 0; i < 16; ++i) s += x[i];
   if (s == 12345.0) out[threadIdx.x] = s;
 }
+// int8 tcgen05: one CTA per SM, one thread issues back-to-back M=128 N=256 K=32
+// MMAs on SMEM-resident operands (constant-offset descriptors, as k_m2l_i8)
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void k_peak_i8(int iters, long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ unsigned long long bar;
+  __shared__ uint32_t tbase;
+  for (int i = threadIdx.x; i < (128 + 256) * 32; i += blockDim.x) sm[i] = (unsigned char)(i * 37);
+  if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t td = tbase;
+  if (threadIdx.x == 0) {
+    auto desc = [](uint32_t a) {
+      return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)8 << 16) | ((uint64_t)16 << 32) | ((uint64_t)1 << 46);
+    };
+    const uint64_t da = desc(su32(sm)), db = desc(su32(sm + 128 * 32));
+    const uint32_t id = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(td),
+                     "l"(da), "l"(db), "r"(id), "r"((it | u) > 0 ? 1 : 0));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    asm volatile("{\n\t.reg .pred P1;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+                 "@!P1 bra W_%=;\n\t}\n" ::"r"(su32(&bar)));
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(td));
+}
 }  // namespace
+
+extern "C" double fdh_tensor_peak_tops(int kind) {
+  if (kind != 0) return 0.0;
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0.0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long* cyc = nullptr;
+  if (cudaMalloc(&cyc, sizeof(long long) * sms) != cudaSuccess) return 0.0;
+  const int smem = (128 + 256) * 32;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  const int iters = 4000;
+  for (int rep = 0; rep < 3; ++rep) {
+    k_peak_i8<<<sms, 128, smem>>>(16, cyc);
+    cudaEventRecord(e0);
+    k_peak_i8<<<sms, 128, smem>>>(iters, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 2.0 * 128 * 256 * 32 * 8.0 * iters * sms;
+    if (ms > 0 && ops / (ms * 1e-3) / 1e12 > best) best = ops / (ms * 1e-3) / 1e12;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(cyc);
+  return cudaGetLastError() == cudaSuccess ? best : 0.0;
+}
 
 extern "C" double fdh_fp64_peak_tflops(int kind) {
   int dev = 0, sms = 0;

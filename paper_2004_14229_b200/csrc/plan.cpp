@@ -654,6 +654,18 @@ void build_m2l(Plan& P) {
   }
   P.m2l_units_exec = exec;
   if (mdbg) {
+    int64_t g8 = 0, g16 = 0;
+    for (int64_t i = 0; i < tot; ++i) {
+      unsigned m8 = 0, m16 = 0;
+      for (int j = 0; j < P.tile_cnt[i]; ++j) {
+        m8 |= 1u << (P.tile_cols[i * TT + j] / 8);
+        m16 |= 1u << (P.tile_cols[i * TT + j] / 16);
+      }
+      g8 += __builtin_popcount(m8);
+      g16 += __builtin_popcount(m16);
+    }
+    std::fprintf(stderr, "[m2l] present 8-target groups %lld (of %lld), 16-target groups %lld (of %lld)\n", (long long)g8,
+                 (long long)(tot * (TT / 8)), (long long)g16, (long long)(tot * std::max(1, TT / 16)));
     int64_t hist[257] = {0};
     for (int64_t i = 0; i < tot; ++i) hist[P.tile_cnt[i]]++;
     std::fprintf(stderr, "[m2l] tiles %lld  tile-keys %lld  units %lld  cnt histogram:", (long long)ntile,

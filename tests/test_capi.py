@@ -36,4 +36,6 @@ def test_library_is_sm100a():
     r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", F.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in r.stdout
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", F.LIB_PATH], capture_output=True, text=True).stdout
-    assert "DMMA.8x8x4" in sass  # the M2L GEMM runs on the FP64 tensor path
+    assert "DMMA.8x8x4" in sass  # the FP64 M2L GEMM (k_m2l_gemm, m = 6) runs on the FP64 tensor path
+    assert "UTCIMMA" in sass      # the int8 digit M2L (k_m2l_i8) runs on tcgen05
+    assert "UBLKCP" in sass       # its coupling digits are moved by bulk async copies

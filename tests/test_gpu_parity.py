@@ -184,6 +184,7 @@ def test_onthefly_coupling_segments(monkeypatch):
     c = CONFIGS[2]
     tg, sr, q = make_inputs(c, nt=60000, ns=50000)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    monkeypatch.setenv("FDH_M2L_IMPL", "dmma")  # the mode is an FP64-path feature (config 4, m = 6)
     y_res = F.DirectionalOperator(*args).apply(q)
     monkeypatch.setenv("FDH_W_ONTHEFLY", "1")
     op = F.DirectionalOperator(*args)
@@ -191,3 +192,48 @@ def test_onthefly_coupling_segments(monkeypatch):
     assert st["w_resident"] == 0 and st["w_segments"] >= 1
     y = op.apply(q)
     assert np.array_equal(y, y_res)  # same matrices, same summation order
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 5])
+def test_m2l_int8_tensor_vs_fp64_dmma(m, monkeypatch):
+    """The int8 tcgen05 M2L (k_m2l_i8: exact products of 7-digit fixed-point
+    operands) against the FP64 DMMA M2L and the oracle on the same inputs."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    op8 = F.DirectionalOperator(*args)
+    assert op8.stats()["m2l_impl"] == 1
+    y8 = op8.apply(q)
+    assert op8.stats()["m2l_i8_ops"] > 0
+    monkeypatch.setenv("FDH_M2L_IMPL", "dmma")
+    opd = F.DirectionalOperator(*args)
+    assert opd.stats()["m2l_impl"] == 0
+    yd = opd.apply(q)
+    yo = oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf).apply(q)
+    e8, ed, e8d = oracle.rel_l2(y8, yo), oracle.rel_l2(yd, yo), oracle.rel_l2(y8, yd)
+    print(f"m={m}: int8 vs oracle {e8:.2e}, dmma vs oracle {ed:.2e}, int8 vs dmma {e8d:.2e}")
+    assert e8 <= TOL and ed <= TOL and e8d <= 1e-13
+    assert np.array_equal(op8.apply(q), y8)  # deterministic: exact integer sums, fixed FP64 chain order
+
+
+def test_m2l_int8_item_split(monkeypatch):
+    """Items capped at 8 keys (many chained items per tile, the int32 overflow
+    guard F of k_m2l_i8) give the same y up to FP64 rounding of the chain."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=40000, ns=40000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    op = F.DirectionalOperator(*args)
+    y = op.apply(q)
+    monkeypatch.setenv("FDH_M2L_FKEYS", "8")
+    op2 = F.DirectionalOperator(*args)
+    assert op2.stats()["m2l_items"] > 2 * op.stats()["m2l_items"]
+    assert oracle.rel_l2(op2.apply(q), y) <= 1e-14
+
+
+def test_m6_keeps_fp64_dmma():
+    """n = 343 nodes per box (m = 6) has no int8 kernel shape: the FP64 DMMA path runs."""
+    rng = np.random.default_rng(7)
+    tg = [rng.random(3000) for _ in range(3)]
+    sr = [rng.random(3000) for _ in range(3)]
+    op = F.DirectionalOperator(tg, sr, (0, 0, 0), (1, 1, 1), 12.0, 32, 6, 1.0, -2)
+    assert op.stats()["m2l_impl"] == 0

@@ -2,6 +2,8 @@
 against the host planner, which is bit-exact with the oracle and the reference's
 own ClusterTree (tests/test_plan.py, tests/test_oracle.py): every export must be
 identical, bit for bit."""
+import os
+
 import numpy as np
 import pytest
 
@@ -18,7 +20,12 @@ def _gpu(gpu_required):
 
 def compare(tg, sr, lo, hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=-2, depth_cap=30, zero_diagonal=0):
     g = F.DirectionalOperator(tg, sr, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal)
-    h = F.DirectionalOperator(tg, sr, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal, plan_only=True)
+    os.environ["FDH_PLAN_I8"] = "1"  # the host plan of the same M2L kernel as the device operator
+    try:
+        h = F.DirectionalOperator(tg, sr, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal,
+                                  plan_only=True)
+    finally:
+        del os.environ["FDH_PLAN_I8"]
     assert g.stats()["gpu_structure"] == 1 and h.stats()["gpu_structure"] == 0
     for w in (0, 1):
         assert np.array_equal(g.tree(w), h.tree(w)), f"tree {w}"
@@ -27,7 +34,8 @@ def compare(tg, sr, lo, hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=-2, depth_cap=3
     assert np.array_equal(g.lplus(), h.lplus())
     assert np.array_equal(g.lminus(), h.lminus())
     sg, sh = g.stats(), h.stats()
-    for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s", "m2l_flops_executed"):
+    for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s", "m2l_tiles", "m2l_items",
+              "m2l_impl", "m2l_flops_executed", "m2l_i8_ops"):
         assert sg[k] == sh[k], k
     return g
 
