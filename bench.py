@@ -139,6 +139,7 @@ def roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traff
             "note": "algorithmic FP64 flop (8 n^2 per admissible block) per second of the M2L kernel, against the "
                     "measured FP64 DMMA peak"}
     if st["m2l_impl"] == 1:
+        import paper_2004_14229_b200 as F
         tops = F.tensor_peak_tops(0)
         # algorithmic int8 work: the 28 digit-pair products (i + j <= 6 of 7 digits) of every
         # real MAC of the complex product (4 n^2 per block, 2 ops per MAC)

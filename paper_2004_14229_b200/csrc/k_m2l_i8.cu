@@ -291,7 +291,7 @@ struct I8Shape {
 
 // dynamic smem: [NST W stages][NST B stages][src table fkeys*TT int32][keys fkeys int32][bars]
 template <int MB, int TT, int KS, int NST, int NGW, int G>
-__global__ void __launch_bounds__(I8Shape<MB, TT, KS, NST, NGW>::THREADS, 1)
+__global__ void __maxnreg__(128)
     k_m2l_i8(const int32_t* __restrict__ item_tile, const int32_t* __restrict__ item_seq,
              const int64_t* __restrict__ item_k0, const int64_t* __restrict__ item_k1,
              const int32_t* __restrict__ tile_nitem, const int32_t* __restrict__ tile_tslot,

@@ -1,4 +1,3 @@
-for c in 2 3 5; do for impl in i8 dmma; do
-FDH_M2L_IMPL=$impl timeout 600 python bench.py --config $c --steps 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg $c $impl', d['ms_per_step'], d['roofline']['gemm_ms'], d['config']['setup_s'])"
+for ov in 0 1; do for fk in 256 128; do
+FDH_M2L_FKEYS=$fk FDH_OVERLAP_NEARFIELD=$ov timeout 300 python bench.py --steps 5 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('ov $ov fk $fk', d['ms_per_step'], r['gemm_ms'], d['phases_ms']['p2p'], r['frac'], r['fp64_equivalent']['ratio'])"
 done; done
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "full_size" 2>&1 | tail -2
