@@ -88,6 +88,7 @@ typedef struct fdh_stats {
   int64_t w_segments;           /* else: per-apply generation segments        */
   int64_t m2l_impl;             /* 0: FP64 DMMA (mma.sync), 1: int8 tcgen05 digit products */
   int64_t m2l_i8_ops;           /* int8 tensor ops (2 per MAC) issued by one M2L (impl 1)  */
+  int64_t nrhs;                 /* right-hand sides per device apply (fdh_create_multi)    */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table
@@ -110,6 +111,17 @@ int fdh_create_shard(const double* tx, const double* ty, const double* tz, int64
                      int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
                      int world, fdh_op** out);
 
+/* Same, for nrhs right-hand sides per apply (nrhs a
+ * power of two in 1..16).  The M2L tiles then pair (target slot, rhs): one
+ * coupling matrix read serves every rhs of a slot, and the near field forms each
+ * kernel value once for up to 8 rhs.  fdh_apply_device on such an operator takes
+ * nrhs vectors (rhs-major: x_dev[r * N_S + k], y_dev[r * N_T + j]). */
+int fdh_create_multi(const double* tx, const double* ty, const double* tz, int64_t nt,
+                     const double* sx, const double* sy, const double* sz, int64_t ns,
+                     const double root_lo[3], const double root_hi[3], double kappa, int n_max,
+                     int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
+                     int world, int nrhs, fdh_op** out);
+
 /* Host-only setup (trees, blocks, directions, work lists; no device state):
  * for introspection and for testing the planner on machines without a GPU.
  * fdh_apply on such an operator returns FDH_ERR_UNSUPPORTED. */
@@ -121,6 +133,10 @@ int fdh_plan_only(const double* tx, const double* ty, const double* tz, int64_t 
 
 /* matvec: y[N_T] = A x[N_S], host buffers, blocking. */
 int fdh_apply(fdh_op* op, const double* x, double* y);
+/* k right-hand sides, host buffers, rhs-major (x[r * N_S + k], y[r * N_T + j]),
+ * run in device batches of nrhs (fdh_create_multi; a short last batch is padded
+ * with zero vectors).  Y = A X with X an N_S x k column-major matrix. */
+int fdh_apply_multi(fdh_op* op, const double* x, int64_t k, double* y);
 /* Device-resident variant: x_dev / y_dev are device pointers (complex128,
  * original order); enqueued on `stream` (cudaStream_t, NULL = the operator's
  * own stream) and not synchronised. */

@@ -26,7 +26,8 @@ LHF_DEFAULT = -2
 
 ERR_ARG, ERR_DOMAIN, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_MEMORY = 1, 2, 3, 4, 5, 6
 PHASES = ["h2d", "s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "d2h"]
-SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_plan_only", "fdh_apply", "fdh_apply_device", "fdh_stream",
+SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_create_multi", "fdh_plan_only", "fdh_apply", "fdh_apply_multi",
+           "fdh_apply_device", "fdh_stream",
            "fdh_set_timing", "fdh_get_stats", "fdh_export_tree", "fdh_export_perm", "fdh_export_lplus",
            "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_structure_digest", "fdh_destroy", "fdh_last_error", "fdh_version",
            "fdh_fp64_peak_tflops", "fdh_tensor_peak_tops"]
@@ -42,7 +43,8 @@ class FdhStats(C.Structure):
                 ("timed_applies", C.c_int64), ("m2l_tiles", C.c_int64), ("m2l_items", C.c_int64),
                 ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
                 ("structure_ms", C.c_double), ("gpu_structure", C.c_int64), ("w_resident", C.c_int64),
-                ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64)]
+                ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64),
+                ("nrhs", C.c_int64)]
 
 
 class FdhError(RuntimeError):
@@ -73,8 +75,10 @@ def lib():
                        C.c_double, C.c_int, C.c_int, C.c_int]
         L.fdh_create.argtypes = create_args + [C.c_int, C.POINTER(C.c_void_p)]
         L.fdh_create_shard.argtypes = create_args + [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.fdh_create_multi.argtypes = create_args + [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.fdh_plan_only.argtypes = create_args + [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.fdh_apply.argtypes = [C.c_void_p, _d, _d]
+        L.fdh_apply_multi.argtypes = [C.c_void_p, _d, C.c_int64, _d]
         L.fdh_apply_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.fdh_stream.argtypes = [C.c_void_p]
         L.fdh_stream.restype = C.c_void_p
@@ -118,7 +122,7 @@ class DirectionalOperator:
     """
 
     def __init__(self, targets, sources, root_lo, root_hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=LHF_DEFAULT,
-                 depth_cap=30, zero_diagonal=False, rank=0, world=1, plan_only=False):
+                 depth_cap=30, zero_diagonal=False, rank=0, world=1, plan_only=False, nrhs=1):
         L = lib()
         self._keep = [_f64(a) for a in (*targets, *sources)]
         tx, ty, tz, sx, sy, sz = self._keep
@@ -131,6 +135,8 @@ class DirectionalOperator:
                 int(m), float(eta2), int(l_hf), int(depth_cap), int(bool(zero_diagonal)))
         if plan_only:
             _chk(L.fdh_plan_only(*args, int(rank), int(world), C.byref(h)))
+        elif nrhs != 1:
+            _chk(L.fdh_create_multi(*args, int(rank), int(world), int(nrhs), C.byref(h)))
         elif world > 1:
             _chk(L.fdh_create_shard(*args, int(rank), int(world), C.byref(h)))
         else:
@@ -156,6 +162,17 @@ class DirectionalOperator:
         return y
 
     matvec = apply
+
+    def apply_multi(self, X, out=None):
+        """k right-hand sides: X complex128[k, N_S] (one rhs per row) -> Y[k, N_T]
+        (SPEC.md:527 `apply(X[N_S x r])`, stored rhs-major)."""
+        X = np.ascontiguousarray(X, dtype=np.complex128)
+        if X.ndim != 2 or X.shape[1] != self.ns:
+            raise FdhError(ERR_DIM, f"X has shape {X.shape}, expected (k, {self.ns})")
+        Y = out if out is not None else np.empty((X.shape[0], self.nt), dtype=np.complex128)
+        _chk(lib().fdh_apply_multi(self.h, X.view(np.float64).ctypes.data_as(_d), X.shape[0],
+                                   Y.view(np.float64).ctypes.data_as(_d)))
+        return Y
 
     def apply_device(self, x_ptr: int, y_ptr: int, stream: int = 0):
         """Device path: raw device pointers (e.g. torch tensor.data_ptr())."""

@@ -103,6 +103,7 @@ struct fdh_op {
   int64_t launches = 0;
   bool applied = false;
   int rank = 0, world = 1;
+  int R = 1;  // right-hand sides per apply (rhs-major vectors)
 
   ~fdh_op() {
     if (st) cudaStreamSynchronize(st);
@@ -277,12 +278,13 @@ void setup_device(fdh_op* o) {
   const int64_t np2 = 2 * (int64_t)P.n_pad;
   const int64_t nkeys = (int64_t)P.key_level.size();
   const int64_t wkey = P.n_pad * m2l_wplanes(P.n_pad) * (int64_t)P.n_k;  // doubles per coupling matrix
-  o->mom = o->alloc<double>((size_t)(P.S.nslots * np2));
-  o->loc = o->alloc<double>((size_t)(P.T.nslots * np2));
+  const int64_t R = o->R = P.prm.nrhs;
+  o->mom = o->alloc<double>((size_t)(R * P.S.nslots * np2));  // [rhs][slot][Re | Im]
+  o->loc = o->alloc<double>((size_t)(R * P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
-  o->ticket = o->alloc<int>((size_t)std::max(o->n_tile, 1));
-  o->q = o->alloc<double2>((size_t)o->ns);
-  o->q4 = o->alloc<double2>((size_t)o->ns);
+  o->ticket = o->alloc<int>((size_t)std::max(2 * o->n_tile, 1));  // int8 m = 6: one chain per M-block group
+  o->q = o->alloc<double2>((size_t)(R * o->ns));
+  o->q4 = o->alloc<double2>((size_t)(R * o->ns));
   {
     std::vector<double2> tab(512);
     const long double pi = 3.141592653589793238462643383279502884L;
@@ -292,57 +294,26 @@ void setup_device(fdh_op* o) {
     }
     o->sctab = o->up(tab);
   }
-  o->yslot = o->alloc<double2>((size_t)o->nt);
-  o->ynear = o->alloc<double2>((size_t)o->nt);
-  o->xin = o->alloc<double2>((size_t)o->ns);
-  o->yout = o->alloc<double2>((size_t)o->nt);
+  o->yslot = o->alloc<double2>((size_t)(R * o->nt));
+  o->ynear = o->alloc<double2>((size_t)(R * o->nt));
+  o->xin = o->alloc<double2>((size_t)(R * o->ns));
+  o->yout = o->alloc<double2>((size_t)(R * o->nt));
   o->flag = o->alloc<int>(1);
   // coupling matrices: resident when they fit (70 % of the free
   // memory), else generated per apply in segments of key chunks (config 4: 240 GB)
   size_t fre = 0, tot = 0;
   CK(cudaMemGetInfo(&fre, &tot));
-  if (P.prm.m2l_impl == 1) {
-    // int8 digits of every coupling matrix, resident (k_m2l_i8.cu); per-level
-    // scales from a first generation pass, digits from a second
-    o->i8 = true;
-    o->nkq = (P.n + 15) / 16 * 16;
-    const int64_t wq = m2l_i8_wbytes_per_key(P.n, o->nkq) * nkeys;
-    const int64_t mq = m2l_i8_mbytes_per_slot(o->nkq) * P.S.nslots;
-    if ((double)(wq + mq) > 0.7 * (double)fre) throw PlanError{-1, "int8 coupling digits do not fit"};
-    o->Wq = o->alloc<int8_t>((size_t)std::max<int64_t>(wq, 16));
-    o->Mq = o->alloc<int8_t>((size_t)std::max<int64_t>(mq, 16));
-    o->lvmax_w = o->alloc<unsigned long long>(kMaxLevels);
-    o->lvmax_v = o->alloc<unsigned long long>(kMaxLevels);
-    CK(cudaMemsetAsync(o->Wq, 0, (size_t)std::max<int64_t>(wq, 16), o->st));
-    CK(cudaMemsetAsync(o->Mq, 0, (size_t)std::max<int64_t>(mq, 16), o->st));
-    CK(cudaMemsetAsync(o->lvmax_w, 0, sizeof(unsigned long long) * kMaxLevels, o->st));
-    o->tile_level_d = o->up(P.tile_level);
-    o->s_slot_level = o->up(P.S.slot_level);
-    const int64_t chunk = 4096;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
-        launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
-                           o->key_dir, pass, o->lvmax_w, o->Wq, P.n, o->nkq);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(o->st));
-    return;
-  }
-  const double wbytes = 8.0 * (double)wkey * (double)nkeys;
   const char* otf = std::getenv("FDH_W_ONTHEFLY");
-  o->w_resident = !(otf && otf[0] == '1') && wbytes <= 0.7 * (double)fre;
-  if (o->w_resident) {
-    o->W = o->alloc<double>((size_t)(nkeys * wkey));
-    const int64_t chunk = 4096;
-    for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
-      launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
-                      o->W, P.n, P.n_pad, P.n_k, 0);
-  } else {
-    // ring of 2 slots, each ~min(8 GB, 20 % of free memory); segments = whole key chunks
-    const double slot_bytes = std::min(8.0e9, 0.2 * (double)fre);
-    int64_t slot_keys = std::max<int64_t>(P.m2l_chunk, (int64_t)(slot_bytes / (8.0 * wkey)) / P.m2l_chunk * P.m2l_chunk);
+  const bool force_otf = otf && otf[0] == '1';
+  // segments of the chunk-major item list for a ring of 2 coupling slots of
+  // slot_keys keys each (whole key chunks): cut where the chunk crosses a slot
+  auto make_segments = [&](int64_t key_bytes) {
+    double slot_bytes = std::min(8.0e9, 0.2 * (double)fre);
+    if (const char* sm = std::getenv("FDH_W_SLOT_MB"))  // testing knob: small slots, many segments
+      slot_bytes = std::max(1.0, std::atof(sm)) * 1048576.0;
+    const int64_t slot_keys =
+        std::max<int64_t>(P.m2l_chunk, (int64_t)(slot_bytes / (double)key_bytes) / P.m2l_chunk * P.m2l_chunk);
     o->w_slot_keys = slot_keys;
-    o->W = o->alloc<double>((size_t)(2 * slot_keys * wkey));
-    // items are sorted by key chunk: cut them where the chunk crosses a slot boundary
     const int64_t ni = (int64_t)P.item_tile.size();
     int64_t i = 0;
     while (i < ni) {
@@ -352,6 +323,58 @@ void setup_device(fdh_op* o) {
       o->segs.push_back({(int)i, (int)j, seg * slot_keys, std::min(nkeys, (seg + 1) * slot_keys)});
       i = j;
     }
+    return slot_keys;
+  };
+  if (P.prm.m2l_impl == 1) {
+    // int8 digits of the coupling matrices (k_m2l_i8.cu): per-level scales from a
+    // first generation pass over every key (setup), digits from a second pass --
+    // at setup for all keys when they fit (70 % of the free memory), else per
+    // apply into a 2-slot ring in segments of key chunks (config 4: 229 GB)
+    o->i8 = true;
+    o->nkq = (P.n + 15) / 16 * 16;
+    const int64_t wkq = m2l_i8_wbytes_per_key(P.n, o->nkq);
+    const int64_t mq = m2l_i8_mbytes_per_slot(o->nkq) * P.S.nslots * R;
+    o->w_resident = !force_otf && (double)(wkq * nkeys + mq) <= 0.7 * (double)fre;
+    if (!o->w_resident && (double)mq > 0.3 * (double)fre) throw PlanError{-1, "int8 moment digits do not fit"};
+    o->Mq = o->alloc<int8_t>((size_t)std::max<int64_t>(mq, 16));
+    o->lvmax_w = o->alloc<unsigned long long>(kMaxLevels);
+    o->lvmax_v = o->alloc<unsigned long long>(kMaxLevels);
+    CK(cudaMemsetAsync(o->Mq, 0, (size_t)std::max<int64_t>(mq, 16), o->st));
+    CK(cudaMemsetAsync(o->lvmax_w, 0, sizeof(unsigned long long) * kMaxLevels, o->st));
+    o->tile_level_d = o->up(P.tile_level);
+    o->s_slot_level = o->up(P.S.slot_level);
+    const int64_t chunk = 4096;
+    if (o->w_resident) {
+      o->Wq = o->alloc<int8_t>((size_t)std::max<int64_t>(wkq * nkeys, 16));
+      CK(cudaMemsetAsync(o->Wq, 0, (size_t)std::max<int64_t>(wkq * nkeys, 16), o->st));
+      for (int pass = 0; pass < 2; ++pass)
+        for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+          launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
+                             o->key_dir, pass, o->lvmax_w, o->Wq, P.n, o->nkq);
+    } else {
+      for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)  // scales only
+        launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
+                           o->key_dir, 0, o->lvmax_w, nullptr, P.n, o->nkq);
+      const int64_t slot_keys = make_segments(wkq);
+      o->Wq = o->alloc<int8_t>((size_t)(2 * slot_keys * wkq));
+      CK(cudaMemsetAsync(o->Wq, 0, (size_t)(2 * slot_keys * wkq), o->st));  // padding rows / K stay zero
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(o->st));
+    return;
+  }
+  const double wbytes = 8.0 * (double)wkey * (double)nkeys;
+  o->w_resident = !force_otf && wbytes <= 0.7 * (double)fre;
+  if (o->w_resident) {
+    o->W = o->alloc<double>((size_t)(nkeys * wkey));
+    const int64_t chunk = 4096;
+    for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+      launch_coupling(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
+                      o->W, P.n, P.n_pad, P.n_k, 0);
+  } else {
+    // ring of 2 slots, each ~min(8 GB, 20 % of free memory); segments = whole key chunks
+    const int64_t slot_keys = make_segments(8 * wkey);
+    o->W = o->alloc<double>((size_t)(2 * slot_keys * wkey));
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(o->st));
@@ -363,33 +386,40 @@ void rec(fdh_op* o, int ph, cudaStream_t st) {
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][ph], st));
 }
 
-// Alg. 4 on the device: x_dev (original order) -> y_dev (original order).
+// Alg. 4 on the device: x_dev (original order) -> y_dev (original order); with
+// R right-hand sides x and y hold R vectors each, rhs-major.  The M2L runs once
+// for all of them (tile columns are (slot, rhs) pairs), the near field forms
+// every kernel value once for up to 8 of them, the other passes run per rhs.
 void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   Plan& P = o->P;
   const int n = P.n, np = P.n_pad;
+  const int R = o->R;
+  const int64_t mstr = P.S.nslots * 2 * (int64_t)np, lstr = P.T.nslots * 2 * (int64_t)np;
   int64_t L = 0;
   CK(cudaEventRecord(o->ev_all[0], st));
   rec(o, FDH_PHASE_H2D, st);
   CK(cudaMemsetAsync(o->flag, 0, sizeof(int), st));
-  launch_gather_charges(st, o->ns, o->perm_s, x, o->q, o->q4);
-  ++L;
+  for (int r = 0; r < R; ++r)
+    launch_gather_charges(st, o->ns, o->perm_s, x + r * o->ns, o->q + r * o->ns, o->q4 + r * o->ns);
+  L += R;
   rec(o, FDH_PHASE_S2M, st);
-  launch_s2m(st, o->dC, o->dirtab, o->n_s2m, o->s2m_slot, o->s2m_level, o->s2m_dir, o->s2m_ci, o->s2m_cj, o->s2m_ck,
-             o->s2m_beg, o->s2m_end, o->sx, o->sy, o->sz, o->q, o->mom, n, np);
-  L += o->n_s2m > 0;
+  for (int r = 0; r < R; ++r)
+    launch_s2m(st, o->dC, o->dirtab, o->n_s2m, o->s2m_slot, o->s2m_level, o->s2m_dir, o->s2m_ci, o->s2m_cj,
+               o->s2m_ck, o->s2m_beg, o->s2m_end, o->sx, o->sy, o->sz, o->q + r * o->ns, o->mom + r * mstr, n, np);
+  L += R * (o->n_s2m > 0);
   rec(o, FDH_PHASE_M2M, st);
   for (int l = (int)o->m2m.size() - 1; l >= 0; --l) {
     const LevelDev& D = o->m2m[l];
     if (D.n == 0) continue;
-    launch_m2m(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.c, D.d, D.crd, o->mom, n, np);
-    ++L;
+    for (int r = 0; r < R; ++r) launch_m2m(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.c, D.d, D.crd, o->mom + r * mstr, n, np);
+    L += R;
   }
   rec(o, FDH_PHASE_M2L, st);
   if (o->overlap_nf) CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
-  CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(P.T.nslots * 2 * np), st));
+  CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(R * lstr), st));
   if (o->n_item > 0 && o->i8) {
-    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
-    launch_mom_quant(st, o->mom, o->s_slot_level, P.S.nslots, n, np, o->nkq, o->lvmax_v, o->Mq);
+    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(2 * o->n_tile), st));
+    launch_mom_quant(st, o->mom, o->s_slot_level, P.S.nslots, n, np, o->nkq, o->lvmax_v, o->Mq, R);
     M2LI8Args a;
     a.n_item = o->n_item;
     a.item_tile = o->item_tile;
@@ -414,10 +444,30 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     a.nkq = o->nkq;
     a.n_pad = np;
     a.fkeys = P.prm.m2l_fkeys;
+    a.n_tile = o->n_tile;
+    const int ng = m2l_i8_groups(n);
     rec(o, FDH_NPHASES + 1, st);
-    if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+    if (o->w_resident) {
+      if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+      L += 2 + ng;
+    } else {
+      const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
+      for (size_t sg = 0; sg < o->segs.size(); ++sg) {
+        const auto& S = o->segs[sg];
+        int8_t* slot = o->Wq + (int64_t)(sg & 1) * o->w_slot_keys * wkq;
+        launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
+                           o->lvmax_w, slot, n, o->nkq, S.key0);
+        M2LI8Args b = a;
+        b.item0 = S.item0;
+        b.n_item = S.item1 - S.item0;
+        b.Wq = slot;
+        b.key_base = S.key0;
+        if (launch_m2l_i8(st, n, P.prm.tile, b) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+        L += 1 + ng;
+      }
+      L += 2;
+    }
     rec(o, FDH_NPHASES + 2, st);
-    L += 3;
   } else if (o->n_item > 0) {
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
     M2LArgs a;
@@ -471,29 +521,31 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
   launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
              o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
-             o->kappa * P.nf_max_dist, o->sctab);
-  L += o->n_leaf > 0;
+             o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt);
+  L += (o->n_leaf > 0) * p2p_launches(R);
   if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
   if (o->overlap_nf) CK(cudaEventRecord(o->ev_nf, o->st2));
   rec(o, FDH_PHASE_L2L, st);
   for (int l = 0; l < (int)o->l2l.size(); ++l) {
     const LevelDev& D = o->l2l[l];
     if (D.n == 0) continue;
-    launch_l2l(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.crd, D.c, D.d, D.e, D.f, o->loc, n, np);
-    ++L;
+    for (int r = 0; r < R; ++r)
+      launch_l2l(st, o->dC, o->dirtab, l, D.n, D.a, D.b, D.crd, D.c, D.d, D.e, D.f, o->loc + r * lstr, n, np);
+    L += R;
   }
   rec(o, FDH_PHASE_L2T, st);
-  if (o->world > 1) CK(cudaMemsetAsync(o->yslot, 0, sizeof(double2) * (size_t)o->nt, st));
+  if (o->world > 1) CK(cudaMemsetAsync(o->yslot, 0, sizeof(double2) * (size_t)(R * o->nt), st));
   if (o->overlap_nf) CK(cudaStreamWaitEvent(st, o->ev_nf, 0));
   rec(o, FDH_NPHASES + 5, st);  // L2T proper starts once the near field is done
-  launch_l2t(st, o->dC, o->dirtab, o->n_leaf, o->l2t_level, o->l2t_slot0, o->l2t_nslot, o->l2t_ci, o->l2t_cj,
-             o->l2t_ck, o->l2t_beg, o->l2t_end, o->tx, o->ty, o->tz, o->tslot_dir, o->loc, o->ynear, o->yslot, n,
-             np);
-  L += o->n_leaf > 0;
+  for (int r = 0; r < R; ++r)
+    launch_l2t(st, o->dC, o->dirtab, o->n_leaf, o->l2t_level, o->l2t_slot0, o->l2t_nslot, o->l2t_ci, o->l2t_cj,
+               o->l2t_ck, o->l2t_beg, o->l2t_end, o->tx, o->ty, o->tz, o->tslot_dir, o->loc + r * lstr,
+               o->ynear + r * o->nt, o->yslot + r * o->nt, n, np);
+  L += R * (o->n_leaf > 0);
   rec(o, FDH_PHASE_P2P, st);  // (P2P itself ran concurrently on st2: see collect_times)
   rec(o, FDH_PHASE_D2H, st);
-  launch_scatter_y(st, o->nt, o->perm_t, o->yslot, y);
-  ++L;
+  for (int r = 0; r < R; ++r) launch_scatter_y(st, o->nt, o->perm_t, o->yslot + r * o->nt, y + r * o->nt);
+  L += R;
   rec(o, FDH_NPHASES, st);
   CK(cudaEventRecord(o->ev_all[1], st));
   CK(cudaGetLastError());
@@ -556,11 +608,13 @@ int guard(F&& f) {
 int create_common(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
                   const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
                   double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
-                  int world, fdh_op** out, bool device = true) {
+                  int world, fdh_op** out, bool device = true, int nrhs = 1) {
   if (!out) return fail(FDH_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (!tx || !ty || !tz || !sx || !sy || !sz || !lo || !hi) return fail(FDH_ERR_ARG, "NULL input pointer");
   if (world < 1 || rank < 0 || rank >= world) return fail(FDH_ERR_ARG, "invalid rank / world");
+  if (nrhs < 1 || nrhs > 16 || (nrhs & (nrhs - 1)) != 0)
+    return fail(FDH_ERR_ARG, "nrhs must be a power of two in 1..16");
   int ndev = 0;
   if (device && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0))
     return fail(FDH_ERR_CUDA, "no CUDA device available");
@@ -577,18 +631,18 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     prm.zero_diagonal = zero_diagonal;
     prm.rank = rank;
     prm.world = world;
+    prm.nrhs = nrhs;
     const char* hs = std::getenv("FDH_HOST_STRUCTURE");  // testing knob: host planner for the structure
     prm.gpu_structure = device && !(hs && hs[0] == '1');
     o->rank = rank;
     o->world = world;
-    // M2L implementation: the int8 tcgen05 kernel where it is compiled (n <= 256
-    // nodes per box, i.e. m <= 5), FP64 DMMA otherwise; FDH_M2L_IMPL=dmma|i8 overrides
+    // M2L implementation: the int8 tcgen05 kernel where it is compiled (n <= 384
+    // nodes per box, i.e. m <= 6), FP64 DMMA otherwise; FDH_M2L_IMPL=dmma overrides
     const int nbox = (m + 1) * (m + 1) * (m + 1);
     const char* mi = std::getenv("FDH_M2L_IMPL");
     const char* pi = std::getenv("FDH_PLAN_I8");  // analysis knob: plan-only operators with the int8 plan
-    const char* otf = std::getenv("FDH_W_ONTHEFLY");  // per-apply coupling generation: FP64 DMMA path only
-    const bool want_i8 = (device || (pi && pi[0] == '1')) && m >= 1 && nbox <= 256 &&
-                         !(mi && std::string(mi) == "dmma") && !(otf && otf[0] == '1');
+    const bool want_i8 = (device || (pi && pi[0] == '1')) && m >= 1 && nbox <= 384 &&
+                         !(mi && std::string(mi) == "dmma");
     if (want_i8) {
       prm.m2l_impl = 1;
       prm.tile = nbox <= 128 ? 32 : 16;
@@ -648,6 +702,14 @@ int fdh_create_shard(const double* tx, const double* ty, const double* tz, int64
                        zero_diagonal, rank, world, out);
 }
 
+int fdh_create_multi(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                     const double* sy, const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3],
+                     double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank,
+                     int world, int nrhs, fdh_op** out) {
+  return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
+                       zero_diagonal, rank, world, out, true, nrhs);
+}
+
 int fdh_plan_only(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx, const double* sy,
                   const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3], double kappa,
                   int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int rank, int world,
@@ -658,22 +720,33 @@ int fdh_plan_only(const double* tx, const double* ty, const double* tz, int64_t 
 
 void fdh_destroy(fdh_op* op) { delete op; }
 
-int fdh_apply(fdh_op* o, const double* x, double* y) {
+int fdh_apply_multi(fdh_op* o, const double* x, int64_t k, double* y) {
   if (!o || !x || !y) return fail(FDH_ERR_ARG, "NULL argument");
+  if (k < 1) return fail(FDH_ERR_ARG, "need at least one right-hand side");
   if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
   return guard([&] {
     CK(cudaSetDevice(o->device));
-    CK(cudaMemcpyAsync(o->xin, x, sizeof(double2) * (size_t)o->ns, cudaMemcpyHostToDevice, o->st));
-    apply_device(o, o->xin, o->yout, o->st);
-    CK(cudaMemcpyAsync(y, o->yout, sizeof(double2) * (size_t)o->nt, cudaMemcpyDeviceToHost, o->st));
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost, o->st));
-    CK(cudaStreamSynchronize(o->st));
-    collect_times(o);
-    if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
-    if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+    const int64_t R = o->R;
+    for (int64_t b = 0; b < k; b += R) {  // batches of R vectors; a short last batch runs with zero vectors
+      const int64_t nb = std::min(R, k - b);
+      if (nb < R)
+        CK(cudaMemsetAsync(o->xin + nb * o->ns, 0, sizeof(double2) * (size_t)((R - nb) * o->ns), o->st));
+      CK(cudaMemcpyAsync(o->xin, x + 2 * b * o->ns, sizeof(double2) * (size_t)(nb * o->ns), cudaMemcpyHostToDevice,
+                         o->st));
+      apply_device(o, o->xin, o->yout, o->st);
+      CK(cudaMemcpyAsync(y + 2 * b * o->nt, o->yout, sizeof(double2) * (size_t)(nb * o->nt),
+                         cudaMemcpyDeviceToHost, o->st));
+      int flag = 0;
+      CK(cudaMemcpyAsync(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost, o->st));
+      CK(cudaStreamSynchronize(o->st));
+      collect_times(o);
+      if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
+      if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+    }
   });
 }
+
+int fdh_apply(fdh_op* o, const double* x, double* y) { return fdh_apply_multi(o, x, 1, y); }
 
 int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream) {
   if (!o || !x_dev || !y_dev) return fail(FDH_ERR_ARG, "NULL argument");
@@ -733,6 +806,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->gpu_structure = P.prm.gpu_structure ? 1 : 0;
   s->w_resident = o->w_resident ? 1 : 0;
   s->w_segments = (int64_t)o->segs.size();
+  s->nrhs = o->R;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

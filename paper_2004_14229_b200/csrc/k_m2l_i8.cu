@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
                                                      const int64_t* __restrict__ key_d,
                                                      const int32_t* __restrict__ key_dir, int pass,
                                                      unsigned long long* __restrict__ lvmax, int8_t* __restrict__ Wq,
-                                                     int n, int nkq, int mb) {
+                                                     int n, int nkq, int mb, int64_t key_base) {
   __shared__ double tn[3][kMaxP], sn[3][kMaxP];
   __shared__ double red[8];
   const int64_t key = key0 + blockIdx.x;
@@ -205,14 +205,17 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
     int8_t dr[KS], di[KS];
     to_digits<KS>(re, ex, dr);
     to_digits<KS>(im, ex, di);
+    // M-block b belongs to group g = b / 2 (blocks {0, 1}, {2}); per (key, K chunk)
+    // the groups are stored one after the other, digit-major inside a group
     const int b = j >> 7, rr = j & 127;
+    const int g = b >> 1, bg = b & 1, mbg = min(2, mb - 2 * g);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int kk = h ? nkq + k : k;  // K index: [Re A | Im A]
       const int ch = kk / kKC, kin = kk % kKC;
-      int8_t* base = Wq + ((key * nch + ch) * KS * mb + b) * (int64_t)kCore + core_off(rr, kin);
+      int8_t* base = Wq + (((key - key_base) * nch + ch) * KS * mb + 2 * g * KS + bg) * (int64_t)kCore + core_off(rr, kin);
 #pragma unroll
-      for (int i = 0; i < KS; ++i) base[(int64_t)i * mb * kCore] = h ? di[i] : dr[i];
+      for (int i = 0; i < KS; ++i) base[(int64_t)i * mbg * kCore] = h ? di[i] : dr[i];
     }
   }
   if (!pass) {
@@ -235,9 +238,10 @@ __device__ __forceinline__ int64_t mq_off(int64_t slot, int nch, int i, int h, i
   return (slot * nch + ch) * (int64_t)(kI8Digits * 4 * 16) + ((i * 2 + (kin >> 4)) * 2 + h) * 16 + (kin & 15);
 }
 __global__ void __launch_bounds__(128) k_mom_max(const double* __restrict__ mom, const int32_t* __restrict__ slot_level,
-                                                 int n, int n_pad, unsigned long long* __restrict__ lvmax) {
+                                                 int n, int n_pad, unsigned long long* __restrict__ lvmax,
+                                                 int64_t nslot1) {
   __shared__ double red[4];
-  const int64_t s = blockIdx.x;
+  const int64_t s = blockIdx.x;  // rhs-major slot id (nrhs > 1): level of slot s % nslot1
   const double* g = mom + s * 2 * n_pad;
   double mx = 0.0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) mx = fmax(mx, fmax(fabs(g[k]), fabs(g[n_pad + k])));
@@ -246,17 +250,17 @@ __global__ void __launch_bounds__(128) k_mom_max(const double* __restrict__ mom,
   __syncthreads();
   if (threadIdx.x == 0) {
     mx = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
-    if (mx > 0.0) atomicMax(lvmax + slot_level[s], (unsigned long long)__double_as_longlong(mx));
+    if (mx > 0.0) atomicMax(lvmax + slot_level[s % nslot1], (unsigned long long)__double_as_longlong(mx));
   }
 }
 template <int KS>
 __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mom,
                                                    const int32_t* __restrict__ slot_level,
                                                    const unsigned long long* __restrict__ lvmax, int n, int n_pad,
-                                                   int nkq, int8_t* __restrict__ Mq) {
+                                                   int nkq, int8_t* __restrict__ Mq, int64_t nslot1) {
   const int64_t s = blockIdx.x;
   const double* g = mom + s * 2 * n_pad;
-  const int ex = level_exp(lvmax, slot_level[s]);
+  const int ex = level_exp(lvmax, slot_level[s % nslot1]);
   const int kp = 2 * nkq;
   const int nch = kp / kKC;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -300,7 +304,8 @@ __global__ void __maxnreg__(128)
              const uint8_t* __restrict__ tile_cnt, const int8_t* __restrict__ Wq, const int8_t* __restrict__ Mq,
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
-             int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys) {
+             int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys, int mb_tot, int grp, int tick_off,
+             int64_t key_base) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int NT = S::THREADS;
@@ -362,7 +367,9 @@ __global__ void __maxnreg__(128)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
         } else {
           mbar_expect_tx(full + s, S::WST);
-          bulk_g2s(wst + s * S::WST, Wq + ((int64_t)keys[kq] * nch + ch) * S::WST, S::WST, full + s);
+          bulk_g2s(wst + s * S::WST,
+                   Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (KS * mb_tot * kCore) + grp * (2 * KS * kCore),
+                   S::WST, full + s);
         }
       }
       __syncwarp();
@@ -473,7 +480,7 @@ __global__ void __maxnreg__(128)
   if (seq > 0) {
     if (tid == 0) {
       long long spins = 0;
-      while (ld_acquire(ticket + tile) != seq) {
+      while (ld_acquire(ticket + tick_off + tile) != seq) {
         __nanosleep(200);
         if (++spins > (1ll << 26)) {  // > ~10 s: report instead of hanging
           atomicOr(err, 2);
@@ -491,7 +498,7 @@ __global__ void __maxnreg__(128)
   const int qw = warp & 3;  // TMEM lane quarter of this warp
 #pragma unroll 1
   for (int b = 0; b < MB && (NGW == 2 || (warp >= 2 && warp < 6)); ++b) {
-    const int row = b * 128 + qw * 32 + lane;
+    const int row = (2 * grp + b) * 128 + qw * 32 + lane;
 #pragma unroll 1
     for (int g = 0; g < NC / 8; ++g) {
       uint32_t r[S::LV][8];
@@ -532,7 +539,7 @@ __global__ void __maxnreg__(128)
   if (!last) {
     __threadfence();
     __syncthreads();
-    if (tid == 0) st_release(ticket + tile, seq + 1);
+    if (tid == 0) st_release(ticket + tick_off + tile, seq + 1);
   }
 }
 
@@ -543,7 +550,7 @@ size_t i8_smem(int fkeys) {
 }
 
 template <int MB, int TT, int NST, int NGW, int G>
-void run_i8(cudaStream_t st, const M2LI8Args& a) {
+void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int grp) {
   using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
   auto kern = k_m2l_i8<MB, TT, kI8Digits, NST, NGW, G>;
   const size_t sm = i8_smem<MB, TT, NST, NGW>(a.fkeys);
@@ -551,14 +558,14 @@ void run_i8(cudaStream_t st, const M2LI8Args& a) {
   kern<<<a.n_item, S::THREADS, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
                                          a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
                                          a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.err, a.item0, a.nkq,
-                                         a.n_pad, a.fkeys);
+                                         a.n_pad, a.fkeys, mb_tot, grp, grp * a.n_tile, a.key_base);
 }
 
 }  // namespace
 
 int m2l_i8_supported(int n, int tile) {
   const int mb = (n + 127) / 128;
-  return (mb == 1 && tile == 32) || (mb == 2 && tile == 16);
+  return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && tile == 16);
 }
 int m2l_i8_fkeys(int nkq) {
   // |digit| <= 64: one key adds at most KS * KP * 64^2 to a level accumulator
@@ -571,18 +578,19 @@ int64_t m2l_i8_mbytes_per_slot(int nkq) { return (int64_t)kI8Digits * 2 * 2 * nk
 
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                         const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
-                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq) {
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int64_t key_base) {
   if (nkeys <= 0) return;
   dim3 grid((unsigned)nkeys, (unsigned)((n + kCplRows - 1) / kCplRows));
   k_coupling_i8<kI8Digits><<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
-                                                 (n + 127) / 128);
+                                                 (n + 127) / 128, key_base);
 }
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
-                      int nkq, unsigned long long* lvmax_v, int8_t* Mq) {
+                      int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs) {
   if (nslots <= 0) return;
   cudaMemsetAsync(lvmax_v, 0, sizeof(unsigned long long) * kMaxLevels, st);
-  k_mom_max<<<(unsigned)nslots, 128, 0, st>>>(mom, slot_level, n, n_pad, lvmax_v);
-  k_mom_quant<kI8Digits><<<(unsigned)nslots, 128, 0, st>>>(mom, slot_level, lvmax_v, n, n_pad, nkq, Mq);
+  const unsigned nb = (unsigned)(nslots * nrhs);
+  k_mom_max<<<nb, 128, 0, st>>>(mom, slot_level, n, n_pad, lvmax_v, nslots);
+  k_mom_quant<kI8Digits><<<nb, 128, 0, st>>>(mom, slot_level, lvmax_v, n, n_pad, nkq, Mq, nslots);
 }
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
@@ -593,13 +601,18 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   }();
   // measured on config 2 (M2L ms): 2 gather warps 38.6, 4: 31.0, 8: 30.2 (G = 1 or 2: same)
   if (mb == 1 && tile == 32) {
-    if (var == 1) run_i8<1, 32, 4, 4, 1>(st, a);
-    else run_i8<1, 32, 4, 8, 1>(st, a);
+    if (var == 1) run_i8<1, 32, 4, 4, 1>(st, a, 1, 0);
+    else run_i8<1, 32, 4, 8, 1>(st, a, 1, 0);
   } else if (mb == 2 && tile == 16) {
-    if (var == 1) run_i8<2, 16, 3, 4, 1>(st, a);
-    else run_i8<2, 16, 3, 8, 1>(st, a);
-  }
-  else return 1;
+    if (var == 1) run_i8<2, 16, 3, 4, 1>(st, a, 2, 0);
+    else run_i8<2, 16, 3, 8, 1>(st, a, 2, 0);
+  } else if (mb == 3 && tile == 16) {
+    // 352 rows (m = 6): TMEM holds 7 levels x 32 columns for two M-blocks only, so
+    // the rows run as two M-block groups {0, 1} and {2}, each its own pass over the
+    // items with its own ticket chain (same moment gather, disjoint W and rows)
+    run_i8<2, 16, 3, 8, 1>(st, a, 3, 0);
+    run_i8<1, 16, 4, 8, 1>(st, a, 3, 1);
+  } else return 1;
   return 0;
 }
 

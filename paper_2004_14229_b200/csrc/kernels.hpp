@@ -31,7 +31,9 @@ void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg,
                 const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
                 const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
                 const double2* q4, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
-                double2* y_slot, int* flag, double max_phase, const double2* sctab);
+                double2* y_slot, int* flag, double max_phase, const double2* sctab, int nrhs = 1,
+                int64_t qstride = 0, int64_t ystride = 0);
+int p2p_launches(int nrhs);
 
 // ---- k_m2l.cu
 void launch_coupling(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
@@ -73,6 +75,8 @@ struct M2LI8Args {
   double* loc = nullptr;
   int* err = nullptr;
   int nkq = 0, n_pad = 0, fkeys = 0;
+  int n_tile = 0;        // ticket chains: one per tile and M-block group (m = 6: 2 groups)
+  int64_t key_base = 0;  // first key of the Wq buffer (on-the-fly segments)
 };
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
@@ -80,9 +84,10 @@ int64_t m2l_i8_wbytes_per_key(int n, int nkq);
 int64_t m2l_i8_mbytes_per_slot(int nkq);
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                         const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
-                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq);
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int64_t key_base = 0);
+inline int m2l_i8_groups(int n) { return (n + 127) / 128 > 2 ? 2 : 1; }  // M-block groups per tile
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
-                      int nkq, unsigned long long* lvmax_v, int8_t* Mq);
+                      int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs = 1);
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a);
 
 }  // namespace fdhelm

@@ -488,6 +488,11 @@ void build_m2l(Plan& P) {
   const TreePlan& T = P.T;
   const TreePlan& S = P.S;
   const int TT = P.prm.tile;
+  // multiple right-hand sides: a tile holds TT / R target slots x R rhs; the
+  // column of (slot i of the tile, rhs r) is i * R + r and refers to the
+  // rhs-major slot id r * nslots + slot (moments / locals stored per rhs)
+  const int R = P.prm.nrhs;
+  if (R < 1 || R > TT || TT % R != 0) throw PlanError{1, "nrhs must divide the M2L tile width " + std::to_string(TT)};
   // pairs (target slot, key, source slot) grouped by target slot: parallel
   // counting pass, prefix, parallel scatter with atomic cursors (the order
   // inside a slot is then fixed by the per-slot sort by key -- keys are unique
@@ -558,7 +563,7 @@ void build_m2l(Plan& P) {
     size_t j = i;
     const int64_t g = gkey(ts[i]);
     while (j < ts.size() && gkey(ts[j]) == g) ++j;
-    for (size_t k = i; k < j; k += TT) tile_first.push_back((int64_t)k);
+    for (size_t k = i; k < j; k += TT / R) tile_first.push_back((int64_t)k);
     i = j;
   }
   tile_first.push_back((int64_t)ts.size());
@@ -587,7 +592,7 @@ void build_m2l(Plan& P) {
     mark.assign(kr, 0);
     int64_t nk = 0;
     for (int64_t i = b; i < e; ++i) {
-      P.tile_tslot[tl * TT + (i - b)] = ts[i];
+      for (int r = 0; r < R; ++r) P.tile_tslot[tl * TT + (i - b) * R + r] = (int32_t)(ts[i] + r * T.nslots);
       for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) {
         nk += !mark[sk[q] - kb];
         mark[sk[q] - kb] = 1;
@@ -616,9 +621,10 @@ void build_m2l(Plan& P) {
     std::vector<int32_t> pos(u.back() - kb + 1, -1);  // key -> position in the union
     for (size_t q = 0; q < u.size(); ++q) pos[u[q] - kb] = (int32_t)q;
     for (int c = 0; c < TT; ++c) {
-      const int32_t t = P.tile_tslot[tl * TT + c];
-      if (t < 0) continue;
-      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) P.tile_src[(base + pos[sk[i] - kb]) * TT + c] = ss[i];
+      const int32_t tv = P.tile_tslot[tl * TT + c];
+      if (tv < 0) continue;
+      const int32_t t = (int32_t)(tv % T.nslots), sr = (int32_t)(tv / T.nslots * S.nslots);
+      for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) P.tile_src[(base + pos[sk[i] - kb]) * TT + c] = ss[i] + sr;
     }
   }
   MTICK("tile src");

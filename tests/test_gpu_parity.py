@@ -194,7 +194,7 @@ def test_onthefly_coupling_segments(monkeypatch):
     assert np.array_equal(y, y_res)  # same matrices, same summation order
 
 
-@pytest.mark.parametrize("m", [1, 2, 4, 5])
+@pytest.mark.parametrize("m", [1, 2, 4, 5, 6])
 def test_m2l_int8_tensor_vs_fp64_dmma(m, monkeypatch):
     """The int8 tcgen05 M2L (k_m2l_i8: exact products of 7-digit fixed-point
     operands) against the FP64 DMMA M2L and the oracle on the same inputs."""
@@ -230,10 +230,32 @@ def test_m2l_int8_item_split(monkeypatch):
     assert oracle.rel_l2(op2.apply(q), y) <= 1e-14
 
 
-def test_m6_keeps_fp64_dmma():
-    """n = 343 nodes per box (m = 6) has no int8 kernel shape: the FP64 DMMA path runs."""
+def test_m6_int8_two_mblock_groups():
+    """n = 343 nodes per box (m = 6): 352 rows run as two M-block groups ({0, 1}
+    and {2}, separate ticket chains); the int8 path is used and matches the oracle."""
     rng = np.random.default_rng(7)
     tg = [rng.random(3000) for _ in range(3)]
     sr = [rng.random(3000) for _ in range(3)]
-    op = F.DirectionalOperator(tg, sr, (0, 0, 0), (1, 1, 1), 12.0, 32, 6, 1.0, -2)
-    assert op.stats()["m2l_impl"] == 0
+    y, yo, op, _ = run_pair(tg, sr, rng.uniform(-1, 1, 3000) + 1j * rng.uniform(-1, 1, 3000), (0, 0, 0), (1, 1, 1),
+                            12.0, 32, 6, 1.0, -2)
+    assert op.stats()["m2l_impl"] == 1 and op.stats()["n_c"] > 0
+    assert oracle.rel_l2(y, yo) <= TOL
+
+
+@pytest.mark.parametrize("m", [4, 6])
+def test_onthefly_coupling_segments_int8(m, monkeypatch):
+    """int8 coupling digits generated per apply in key-chunk segments (config 4:
+    229 GB of digits do not fit) against digits generated once at setup: bitwise."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=40000, ns=30000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    op_res = F.DirectionalOperator(*args)
+    assert op_res.stats()["m2l_impl"] == 1 and op_res.stats()["w_resident"] == 1
+    y_res = op_res.apply(q)
+    monkeypatch.setenv("FDH_W_ONTHEFLY", "1")
+    monkeypatch.setenv("FDH_W_SLOT_MB", "64")  # several segments at this size
+    op = F.DirectionalOperator(*args)
+    st = op.stats()
+    assert st["m2l_impl"] == 1 and st["w_resident"] == 0 and st["w_segments"] >= 2
+    y = op.apply(q)
+    assert np.array_equal(y, y_res)  # same digits and scales, same summation order
