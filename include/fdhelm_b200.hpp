@@ -30,6 +30,7 @@ struct Params {
   int l_hf = FDH_LHF_DEFAULT;
   int depth_cap = 30;
   bool zero_diagonal = false;
+  int nrhs = 1;            // right-hand sides per device batch (power of two, <= 16)
 };
 
 inline void check(int rc) {
@@ -76,9 +77,9 @@ class DirectionalOperator {
       : nt_(tx.size()), ns_(sx.size()) {
     if (ty.size() != nt_ || tz.size() != nt_ || sy.size() != ns_ || sz.size() != ns_)
       throw std::invalid_argument("coordinate arrays of one point set differ in length");
-    check(fdh_create(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(), (int64_t)ns_,
-                     root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap, p.zero_diagonal ? 1 : 0,
-                     1, &op_));
+    check(fdh_create_multi(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(),
+                           (int64_t)ns_, root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap,
+                           p.zero_diagonal ? 1 : 0, 0, 1, p.nrhs, &op_));
   }
   DirectionalOperator(const DirectionalOperator&) = delete;
   DirectionalOperator& operator=(const DirectionalOperator&) = delete;
@@ -93,6 +94,13 @@ class DirectionalOperator {
     std::vector<Complex> y(nt_);
     apply(x, y);
     return y;
+  }
+  // Y = A X for k right-hand sides, X column-major N_S x k
+  // (column r = x[r * N_S ...]), Y column-major N_T x k.
+  void apply_multi(std::span<const Complex> X, std::span<Complex> Y, int64_t k) {
+    if (k < 1 || X.size() != ns_ * (size_t)k || Y.size() != nt_ * (size_t)k)
+      throw std::invalid_argument("matvec: dimension mismatch");
+    check(fdh_apply_multi(op_, reinterpret_cast<const double*>(X.data()), k, reinterpret_cast<double*>(Y.data())));
   }
   fdh_stats stats() const {
     fdh_stats s{};
