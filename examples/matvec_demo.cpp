@@ -65,7 +65,7 @@ int main(int argc, char** argv) {
       dm += std::norm(Y[j] - y[j]) + std::norm(Y[n + j] - 2.0 * y[j]);
       dn += 5.0 * std::norm(y[j]);
     }
-    if (std::sqrt(dm / dn) > 1e-13) {
+    if (std::sqrt(dm / dn) > 1e-12) {  // int8 M2L: the batch shares one moment scale per level
       std::fprintf(stderr, "multi-rhs apply differs from single applies: %.3e\n", std::sqrt(dm / dn));
       return 4;
     }

@@ -2,9 +2,11 @@
 fdh_create_multi / fdh_apply_multi against one single-vector apply per column and
 against the CPU oracle.  M2L tile columns become (target slot, rhs) pairs and the
 near field forms each kernel value once for up to 8 vectors, so the summation
-order inside the M2L differs from the single-vector plan: columns agree with the
-single applies to FP64 rounding (<= 1e-13 relative), and with the oracle to the
-parity bound 1e-12 (BASELINE.json north_star)."""
+order inside the M2L differs from the single-vector plan, and on the int8 M2L the
+per-level moment scale is shared by the vectors of a batch (a different digit
+rounding): columns agree with the single applies to the int8 path's own error
+level (measured <= 2.7e-13 at m = 6, bound 5e-13; FP64 DMMA path 1e-13), and with
+the oracle to the parity bound 1e-12 (BASELINE.json north_star)."""
 import numpy as np
 import pytest
 
@@ -14,6 +16,7 @@ from paper_2004_14229_b200.configs import CONFIGS, make_inputs
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
+I8 = 5e-13  # int8 M2L vs int8 M2L with different digit roundings
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -38,7 +41,7 @@ def test_multi_rhs_vs_single(m, nrhs):
     Y = opm.apply_multi(X)
     op1 = F.DirectionalOperator(*args)
     for r in range(X.shape[0]):
-        assert oracle.rel_l2(Y[r], op1.apply(X[r])) <= 1e-13, r
+        assert oracle.rel_l2(Y[r], op1.apply(X[r])) <= I8, r
     o = oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
     for r in (0, nrhs):
         assert oracle.rel_l2(Y[r], o.apply(X[r])) <= TOL
@@ -69,7 +72,7 @@ def test_multi_rhs_zero_diagonal_and_linearity():
     Y = op.apply_multi(np.stack([x, yv, 2 * x + 1j * yv]))
     o = oracle.Oracle(pts, pts, (0, 0, 0), (1, 1, 1), 10.0, 32, 4, 1.0, -2, 30, True)
     assert oracle.rel_l2(Y[0], o.apply(x)) <= TOL
-    assert oracle.rel_l2(Y[2], 2 * Y[0] + 1j * Y[1]) <= 1e-13
+    assert oracle.rel_l2(Y[2], 2 * Y[0] + 1j * Y[1]) <= TOL  # the batch shares one scale: x, y lose ~1 bit
 
 
 def test_multi_rhs_single_apply_and_errors():
@@ -78,7 +81,7 @@ def test_multi_rhs_single_apply_and_errors():
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
     op = F.DirectionalOperator(*args, nrhs=4)
     y1 = F.DirectionalOperator(*args).apply(q)
-    assert oracle.rel_l2(op.apply(q), y1) <= 1e-13  # fdh_apply = one vector + zero padding
+    assert oracle.rel_l2(op.apply(q), y1) <= I8  # fdh_apply = one vector + zero padding
     with pytest.raises(F.FdhError):
         F.DirectionalOperator(*args, nrhs=3)  # not a power of two
     with pytest.raises(F.FdhError):
