@@ -198,6 +198,25 @@ def roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traff
             "gemm_ms": gemm_ms, "share_of_step": share}
 
 
+def hbm_passes(st, ph):
+    """S2M / M2M / L2L / L2T against the measured HBM copy bandwidth (MEASURED_PEAKS.json
+    hbm_gbs): algorithmic bytes of SURVEY.md 8(d) (fdh_stats.hbm_bytes) / phase time."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+        src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak, src = 7700.0, "fallback: nominal B200 HBM3e (MEASURED_PEAKS.json absent)"
+    out = {"peak_gbs": peak, "peak_source": src,
+           "note": "< 1 % of the step; per (box, direction) work items of 15-60 points are latency / FP64-bound "
+                   "(sincos, Lagrange cardinals per point), not bandwidth-bound, at these sizes"}
+    for k in ("s2m", "m2m", "l2l", "l2t"):
+        b, ms = st["hbm_bytes"][k], ph.get(k, 0.0)
+        gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else None
+        out[k] = {"bytes": b, "ms": ms, "achieved_gbs": gbs, "frac": gbs / peak if gbs else None}
+    return out
+
+
 def run_reference(args, c, rank, world):
     """--impl reference: the reference algorithm on the host cores (oracle port)."""
     if rank != 0:
@@ -352,7 +371,12 @@ def run_ours(args, c, rank, world, local_rank):
         "roofline": roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traffic),
         "phases_ms": ph,
         "p2p": {"pairs": st["m_d"], "ms": p2p_ms,
-                "tflops_24flop_per_pair": 24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else None},
+                "tflops_24flop_per_pair": 24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else None,
+                "frac_of_fp64_peak": (24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 / peak
+                                      if (p2p_ms > 0 and peak) else None),
+                "note": "24 flop per pair (SURVEY.md 8(d), rsqrt and sincos counted as 1 each); the kernel issues "
+                        "~35 FP64 instructions per pair (SASS), FP64 pipe ~67 % active (profiles/r01_ncu_p2p_fast.json)"},
+        "hbm_passes": hbm_passes(st, ph),
         "counters": {k: st[k] for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s",
                                         "depth_t", "depth_s")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.ns, "d2h_bytes_per_step": 16 * c.nt,

@@ -44,7 +44,7 @@ class FdhStats(C.Structure):
                 ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
                 ("structure_ms", C.c_double), ("gpu_structure", C.c_int64), ("w_resident", C.c_int64),
                 ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64),
-                ("nrhs", C.c_int64)]
+                ("nrhs", C.c_int64), ("hbm_bytes", C.c_int64 * 4)]
 
 
 class FdhError(RuntimeError):
@@ -187,7 +187,8 @@ class DirectionalOperator:
     def stats(self) -> dict:
         s = FdhStats()
         _chk(lib().fdh_get_stats(self.h, C.byref(s)))
-        d = {f: getattr(s, f) for f, _ in FdhStats._fields_ if f != "phase_ms"}
+        d = {f: getattr(s, f) for f, _ in FdhStats._fields_ if f not in ("phase_ms", "hbm_bytes")}
+        d["hbm_bytes"] = dict(zip(("s2m", "m2m", "l2l", "l2t"), list(s.hbm_bytes)))
         d["phase_ms"] = dict(zip(PHASES, list(s.phase_ms)))
         return d
 

@@ -817,6 +817,23 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
     s->m2l_flops_executed = 0;
     s->m2l_i8_ops = 2 * (int64_t)P.tile_keys.size() * ((P.n + 127) / 128) * 128 * (2 * nkq) * cols;
   }
+  // algorithmic HBM bytes of the transfer passes per rhs: 16 n B per
+  // moment / local vector read or written, 40 B per source point (S2M), 24 + 32 B per
+  // target point (L2T: point read, y read-modify-write)
+  const int64_t v16 = 16 * (int64_t)P.n;
+  s->hbm_bytes[0] = 40 * (int64_t)P.S.perm.size() + v16 * (int64_t)P.s2m_slot.size();
+  int64_t m2m = 0, l2l = 0, l2t = 0;
+  for (size_t l = 0; l < P.m2m_parent.size(); ++l) {
+    m2m += (int64_t)P.m2m_parent[l].size();
+    for (int32_t c : P.m2m_child[l]) m2m += c >= 0;
+  }
+  for (size_t l = 0; l < P.l2l_child.size(); ++l) l2l += (int64_t)P.l2l_pslot[l].size() + 2 * (int64_t)P.l2l_child[l].size();
+  for (size_t i = 0; i < P.l2t_nslot.size(); ++i) l2t += P.l2t_nslot[i];
+  int64_t nt_own = 0;
+  for (size_t i = 0; i < P.l2t_begin.size(); ++i) nt_own += (int64_t)P.l2t_end[i] - P.l2t_begin[i];
+  s->hbm_bytes[1] = v16 * m2m;
+  s->hbm_bytes[2] = v16 * l2l;
+  s->hbm_bytes[3] = v16 * l2t + 56 * nt_own;
   return FDH_OK;
 }
 
