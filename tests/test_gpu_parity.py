@@ -199,7 +199,8 @@ def test_m2l_int8_tensor_vs_fp64_dmma(m, monkeypatch):
     """The int8 tcgen05 M2L (k_m2l_i8: exact products of 7-digit fixed-point
     operands) against the FP64 DMMA M2L and the oracle on the same inputs."""
     c = CONFIGS[2]
-    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    nt, ns = (30000, 25000) if m <= 5 else (15000, 12000)  # the oracle's cost grows with (m+1)^6
+    tg, sr, q = make_inputs(c, nt=nt, ns=ns)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
     op8 = F.DirectionalOperator(*args)
     assert op8.stats()["m2l_impl"] == 1
@@ -248,7 +249,7 @@ def test_onthefly_coupling_segments_int8(m, monkeypatch):
     """int8 coupling digits generated per apply in key-chunk segments (config 4:
     229 GB of digits do not fit) against digits generated once at setup: bitwise."""
     c = CONFIGS[2]
-    tg, sr, q = make_inputs(c, nt=40000, ns=30000)
+    tg, sr, q = make_inputs(c, nt=40000 if m <= 4 else 20000, ns=30000 if m <= 4 else 15000)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
     op_res = F.DirectionalOperator(*args)
     assert op_res.stats()["m2l_impl"] == 1 and op_res.stats()["w_resident"] == 1
