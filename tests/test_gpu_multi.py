@@ -32,7 +32,7 @@ def _charges(k, ns, seed):
 @pytest.mark.parametrize("m,nrhs", [(4, 2), (4, 8), (4, 16), (5, 4), (6, 2)])
 def test_multi_rhs_vs_single(m, nrhs):
     c = CONFIGS[2]
-    nt, ns = (30000, 25000) if m <= 4 else (12000, 10000)  # the oracle's cost grows with (m+1)^6
+    nt, ns = (15000, 12000) if m <= 4 else (12000, 10000)  # the oracle's cost grows with (m+1)^6
     tg, sr, _ = make_inputs(c, nt=nt, ns=ns)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
     X = _charges(nrhs + 1, ns, 7 + m)  # the last device batch is padded with zero vectors
