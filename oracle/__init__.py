@@ -77,6 +77,9 @@ def lib():
         L.orc_dense_rows.argtypes = [_d, _d, _d, _i64, C.c_int64, _d, _d, _d, C.c_int64, _d, C.c_double, C.c_int, _d]
         L.orc_kernel.argtypes = [_d, C.c_double, _d]
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_create_sampled.argtypes = [_d, _d, _d, C.c_int64, _d, _d, _d, C.c_int64, _d, _d, C.c_double, C.c_int,
+                                         C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _i64, C.c_int64,
+                                         C.POINTER(C.c_void_p)]
         _lib = L
     return _lib
 
@@ -137,15 +140,23 @@ class Oracle:
     """CPU oracle operator (Alg. 1-4 restated)."""
 
     def __init__(self, targets, sources, root_lo, root_hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=-2,
-                 depth_cap=30, zero_diagonal=0, structure_only=False):
+                 depth_cap=30, zero_diagonal=0, structure_only=False, sample_leaves=None):
+        """sample_leaves: canonical target-leaf indices -> sampled-structure operator
+        (orc_create_sampled: partition below those leaves' ancestors only, coupling
+        generated per block); only apply_sampled on the same leaves is defined."""
         L = lib()
         self._keep = [_f64(a) for a in (*targets, *sources)]
         tx, ty, tz, sx, sy, sz = self._keep
         lo, hi = _f64(root_lo), _f64(root_hi)
         h = C.c_void_p()
-        fn = L.orc_create_structure if structure_only else L.orc_create
-        _chk(fn(_p(tx), _p(ty), _p(tz), len(tx), _p(sx), _p(sy), _p(sz), len(sx), _p(lo), _p(hi), float(kappa),
-                int(n_max), int(m), float(eta2), int(l_hf), int(depth_cap), int(zero_diagonal), C.byref(h)))
+        args = (_p(tx), _p(ty), _p(tz), len(tx), _p(sx), _p(sy), _p(sz), len(sx), _p(lo), _p(hi), float(kappa),
+                int(n_max), int(m), float(eta2), int(l_hf), int(depth_cap), int(zero_diagonal))
+        if sample_leaves is not None:
+            self._lv = np.ascontiguousarray(sample_leaves, dtype=np.int64)
+            _chk(L.orc_create_sampled(*args, _pi(self._lv), len(self._lv), C.byref(h)))
+        else:
+            fn = L.orc_create_structure if structure_only else L.orc_create
+            _chk(fn(*args, C.byref(h)))
         self.h = h
         self.nt, self.ns = len(tx), len(sx)
 

@@ -385,6 +385,11 @@ struct Op {
   int64_t nslotT = 0, nslotS = 0;
   std::vector<int64_t> lp_ptr, lm_ptr;  // CSR by target node
   int64_t M_D = 0, M_D_zero = 0;
+  // sampled-structure mode (orc_create_sampled): the block partition is refined
+  // only below target boxes that are ancestors of the sampled leaves, and the
+  // coupling matrices are generated per block in the M2L instead of stored
+  std::vector<char> need_t;  // empty = every target box
+  bool onthefly = false;
 };
 
 bool admissible(const Op& op, int32_t t, int32_t s) {
@@ -413,7 +418,7 @@ void refine_block(Op& op, int32_t t, int32_t s, std::vector<std::pair<int32_t, i
   }
   if (!adm_ts) {
     for (int a = 0; a < 8; ++a) {
-      if (nt.child[a] < 0) continue;
+      if (nt.child[a] < 0 || (!op.need_t.empty() && !op.need_t[nt.child[a]])) continue;
       for (int b = 0; b < 8; ++b) {
         if (ns.child[b] < 0) continue;
         refine_block(op, nt.child[a], ns.child[b], adm);
@@ -659,7 +664,11 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
   }
   // (iii) M2L: g~_{t,c} += A_{c,t x s} v~_{s,c}; owner computes over t
   const int64_t nT = (int64_t)T.nodes.size();
-#pragma omp parallel for schedule(dynamic, 4)
+#pragma omp parallel
+  {
+  std::vector<cplx> Abuf(op.onthefly ? (size_t)n * n : 0);
+  int32_t Akey = -1;
+#pragma omp for schedule(dynamic, 4)
   for (int64_t t = 0; t < nT; ++t) {
     if (!need[t]) continue;
     for (int64_t b = op.lp_ptr[t]; b < op.lp_ptr[t + 1]; ++b) {
@@ -667,7 +676,21 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
       const int32_t tdi = find_dir(op.dT[t], bk.dir), sdi = find_dir(op.dS[bk.s], bk.dir);
       cplx* out = &loc[(size_t)(op.slotT[t] + tdi) * n];
       const cplx* in = &mom[(size_t)(op.slotS[bk.s] + sdi) * n];
-      const cplx* A = &op.coupling[(size_t)bk.key * n * n];
+      const cplx* A;
+      if (op.onthefly) {  // the same deterministic coupling_matrix as build_coupling
+        if (bk.key != Akey) {
+          const auto& key = op.keys[bk.key];
+          const int kl = std::get<0>(key);
+          double c[3];
+          dir_vec(kl, op.lhf, op.key_dir[bk.key], c);
+          coupling_matrix(op.m, op.kappa, op.T.side[kl].data(), std::get<1>(key), std::get<2>(key),
+                          std::get<3>(key), c, Abuf.data());
+          Akey = bk.key;
+        }
+        A = Abuf.data();
+      } else {
+        A = &op.coupling[(size_t)bk.key * n * n];
+      }
       for (int j = 0; j < n; ++j) {
         cplx acc(0, 0);
         const cplx* Aj = A + (size_t)j * n;
@@ -675,6 +698,7 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
         out[j] += acc;
       }
     }
+  }
   }
   // (iv) L2L, levels 0 .. p(T_T)-1: g~_{t',c'} += E_{t',c} g~_{t,c}
   for (int l = 0; l < T.depth; ++l) {
@@ -806,7 +830,7 @@ int orc_set_threads(int n) {
 static int create_impl(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
                        const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
                        double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal,
-                       bool coupling, orc_op** out) {
+                       bool coupling, orc_op** out, const int64_t* sample = nullptr, int64_t nsample = 0) {
   *out = nullptr;
   return guard([&] {
     if (!(kappa > 0.0) || !std::isfinite(kappa)) throw Err(E_ARG, "wave number must be positive and finite");
@@ -825,9 +849,20 @@ static int create_impl(const double* tx, const double* ty, const double* tz, int
       op.zero_diag = zero_diagonal;
       op.T.build(tx, ty, tz, nt, lo, hi, n_max, depth_cap);
       op.S.build(sx, sy, sz, ns, lo, hi, n_max, depth_cap);
+      if (sample) {
+        op.need_t.assign(op.T.nodes.size(), 0);
+        for (int64_t i = 0; i < nsample; ++i) {
+          if (sample[i] < 0 || sample[i] >= (int64_t)op.T.leaves.size()) throw Err(E_ARG, "leaf index out of range");
+          for (int32_t id = op.T.leaves[sample[i]]; id >= 0; id = op.T.nodes[id].parent) op.need_t[id] = 1;
+        }
+        op.need_t[0] = 1;
+        op.onthefly = true;
+        coupling = false;
+      }
       build_structure(op);
       op.with_coupling = coupling;
       if (coupling) build_coupling(op);
+      else op.Eref = transfer_ref(op.m);
     } catch (...) {
       delete o;
       throw;
@@ -849,6 +884,13 @@ int orc_create_structure(const double* tx, const double* ty, const double* tz, i
   return create_impl(tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal,
                      false, out);
 }
+int orc_create_sampled(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                       const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
+                       double kappa, int n_max, int m, double eta2, int l_hf, int depth_cap, int zero_diagonal,
+                       const int64_t* leaf_idx, int64_t nleaf, orc_op** out) {
+  return create_impl(tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, kappa, n_max, m, eta2, l_hf, depth_cap, zero_diagonal,
+                     false, out, leaf_idx, nleaf);
+}
 void orc_destroy(orc_op* op) { delete op; }
 
 int orc_apply(orc_op* o, const double* x, double* y) {
@@ -859,7 +901,10 @@ int orc_apply(orc_op* o, const double* x, double* y) {
 }
 int orc_apply_sampled(orc_op* o, const double* x, const int64_t* leaf_idx, int64_t nleaf, double* y) {
   return guard([&] {
-    if (!o->op.with_coupling) throw Err(E_ARG, "operator built without coupling matrices");
+    if (!o->op.with_coupling && !o->op.onthefly) throw Err(E_ARG, "operator built without coupling matrices");
+    for (int64_t i = 0; i < nleaf && !o->op.need_t.empty(); ++i)
+      if (leaf_idx[i] >= 0 && leaf_idx[i] < (int64_t)o->op.T.leaves.size() && !o->op.need_t[o->op.T.leaves[leaf_idx[i]]])
+        throw Err(E_ARG, "leaf was not sampled at orc_create_sampled");
     std::vector<char> mask(o->op.T.leaves.size(), 0);
     for (int64_t i = 0; i < nleaf; ++i) {
       if (leaf_idx[i] < 0 || leaf_idx[i] >= (int64_t)mask.size()) throw Err(E_ARG, "leaf index out of range");

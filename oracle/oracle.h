@@ -56,6 +56,17 @@ int orc_create_structure(const double* tx, const double* ty, const double* tz, i
                          const double root_lo[3], const double root_hi[3], double kappa,
                          int n_max, int m, double eta2, int l_hf, int depth_cap,
                          int zero_diagonal, orc_op** out);
+/* Sampled-structure operator for sizes whose full L+ / coupling set does not fit
+ * in host memory (config 4): trees in full, block partition only below the target
+ * boxes on the paths root -> sampled leaf (leaf_idx in canonical leaf order),
+ * moments only for the (box, direction) slots those blocks need, coupling
+ * matrices generated per block.  orc_apply_sampled with the same leaves gives the
+ * same values as a full operator's orc_apply_sampled. */
+int orc_create_sampled(const double* tx, const double* ty, const double* tz, int64_t nt,
+                       const double* sx, const double* sy, const double* sz, int64_t ns,
+                       const double lo[3], const double hi[3], double kappa, int n_max, int m,
+                       double eta2, int l_hf, int depth_cap, int zero_diagonal,
+                       const int64_t* leaf_idx, int64_t nleaf, orc_op** out);
 void orc_destroy(orc_op* op);
 const char* orc_last_error(void);
 int orc_set_threads(int n);

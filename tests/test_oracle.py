@@ -232,3 +232,22 @@ def test_zero_diagonal():
     assert o.stats()["M_D_zero"] == 512
     yd = oracle.dense_rows(g, g, q, 0.8, np.arange(512), zero_diagonal=1)
     assert oracle.rel_l2(y, yd) < 1e-2
+
+
+@pytest.mark.parametrize("cfg,m", [(1, 4), (2, 3)])
+def test_sampled_structure_oracle_matches_full(cfg, m):
+    """orc_create_sampled (partition only below the sampled leaves' ancestors,
+    coupling generated per block; used for config 4, whose full L+ and coupling
+    set do not fit in host memory) gives bitwise the rows of the full oracle."""
+    c = CONFIGS[cfg]
+    nt, ns = (None, None) if cfg == 1 else (30000, 25000)
+    tg, sr, q = make_inputs(c) if cfg == 1 else make_inputs(c, nt=nt, ns=ns)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32 if cfg == 2 else c.n_max, m, c.eta2, c.l_hf)
+    full = oracle.Oracle(*args)
+    nl = full.leaf_count(0)
+    leaves = np.unique(np.concatenate([[0, nl - 1], np.random.default_rng(cfg).choice(nl, 4, replace=False)]))
+    rows, yf = full.apply_sampled(q, leaves)
+    samp = oracle.Oracle(*args, sample_leaves=leaves)
+    rows2, ys = samp.apply_sampled(q, leaves)
+    assert np.array_equal(rows, rows2)
+    assert np.array_equal(yf, ys)
