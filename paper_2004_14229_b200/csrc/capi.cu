@@ -96,6 +96,7 @@ struct fdh_op {
   cudaEvent_t ev_q = nullptr, ev_nf = nullptr;
   double2* ynear = nullptr;
   bool overlap_nf = false;
+  int nsm = 148, nf_ctas = 1;  // persistent near-field grid when overlapped
   int ring_n = 0;                                 // applies recorded since the last reset
   cudaEvent_t ev[FDH_NPHASES + 1] = {};
   cudaEvent_t ev_all[2] = {};
@@ -154,6 +155,8 @@ void setup_device(fdh_op* o) {
   CK(cudaStreamCreateWithFlags(&o->st, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&o->st2, cudaStreamNonBlocking));
   if (const char* e = std::getenv("FDH_OVERLAP_NEARFIELD")) o->overlap_nf = e[0] == '1';
+  CK(cudaDeviceGetAttribute(&o->nsm, cudaDevAttrMultiProcessorCount, o->device));
+  if (const char* e = std::getenv("FDH_NF_CTAS")) o->nf_ctas = std::max(1, std::atoi(e));  // tuning knob
   CK(cudaEventCreateWithFlags(&o->ev_q, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&o->ev_nf, cudaEventDisableTiming));
   for (auto& e : o->ev) CK(cudaEventCreate(&e));
@@ -415,7 +418,26 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     L += R;
   }
   rec(o, FDH_PHASE_M2L, st);
-  if (o->overlap_nf) CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
+  // near field (vi).  Sequential (default for the FP64 DMMA M2L, which shares the
+  // FP64 pipe with it): on the main stream after the M2L.  overlap_nf (default for
+  // the int8 M2L: tensor pipe vs FP64 pipe): launched on the second stream BEFORE
+  // the M2L as a persistent grid of nf_ctas CTAs per SM, so one near-field CTA
+  // (20 KB shared memory, 128 threads) is resident beside each M2L CTA and the
+  // two run concurrently on different pipes.
+  auto near_field = [&](cudaStream_t snf, int grid) {
+    if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
+    launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
+               o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
+               o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt, grid);
+    L += (o->n_leaf > 0) * p2p_launches(R);
+    if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
+  };
+  if (o->overlap_nf) {
+    CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
+    CK(cudaStreamWaitEvent(o->st2, o->ev_q, 0));
+    near_field(o->st2, o->nsm * o->nf_ctas);
+    CK(cudaEventRecord(o->ev_nf, o->st2));
+  }
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(R * lstr), st));
   if (o->n_item > 0 && o->i8) {
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(2 * o->n_tile), st));
@@ -512,19 +534,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     rec(o, FDH_NPHASES + 2, st);
     L += 1;
   }
-  // near field (vi).  Default: on the main stream right after the M2L GEMM (the
-  // GEMM keeps the whole GPU, phases are sequential).  overlap_nf: on the second
-  // stream, concurrent with the GEMM (its CTAs take the slots the GEMM leaves
-  // free) -- measured 0.75 % faster overall on cfg2, the GEMM itself 5 % slower.
-  cudaStream_t snf = o->overlap_nf ? o->st2 : st;
-  if (o->overlap_nf) CK(cudaStreamWaitEvent(o->st2, o->ev_q, 0));
-  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
-  launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
-             o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
-             o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt);
-  L += (o->n_leaf > 0) * p2p_launches(R);
-  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
-  if (o->overlap_nf) CK(cudaEventRecord(o->ev_nf, o->st2));
+  if (!o->overlap_nf) near_field(st, 0);
   rec(o, FDH_PHASE_L2L, st);
   for (int l = 0; l < (int)o->l2l.size(); ++l) {
     const LevelDev& D = o->l2l[l];

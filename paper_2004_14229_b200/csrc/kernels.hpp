@@ -32,7 +32,7 @@ void launch_p2p(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg,
                 const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
                 const double2* q4, const uint32_t* perm_t, const uint32_t* perm_s, int zero_diag,
                 double2* y_slot, int* flag, double max_phase, const double2* sctab, int nrhs = 1,
-                int64_t qstride = 0, int64_t ystride = 0);
+                int64_t qstride = 0, int64_t ystride = 0, int grid = 0);
 int p2p_launches(int nrhs);
 
 // ---- k_m2l.cu
