@@ -666,7 +666,7 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
         setup_device(o);
       } catch (const PlanError& e) {
         if (e.code != -1) throw;
-        // int8 digits do not fit: rebuild with the FP64 DMMA path
+        // int8 moment digits do not fit: rebuild with the FP64 DMMA path
         delete o;
         o = new fdh_op;
         o->rank = rank;
