@@ -90,6 +90,7 @@ typedef struct fdh_stats {
   int64_t m2l_i8_ops;           /* int8 tensor ops (2 per MAC) issued by one M2L (impl 1)  */
   int64_t nrhs;                 /* right-hand sides per device apply (fdh_create_multi)    */
   int64_t hbm_bytes[4];         /* algorithmic HBM bytes per rhs of S2M, M2M, L2L, L2T     */
+  int64_t graph_replays;        /* applies run as a replay of the captured CUDA graph      */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

@@ -44,7 +44,7 @@ class FdhStats(C.Structure):
                 ("m2l_chunk", C.c_int64), ("shard_cost", C.c_double), ("total_cost", C.c_double),
                 ("structure_ms", C.c_double), ("gpu_structure", C.c_int64), ("w_resident", C.c_int64),
                 ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64),
-                ("nrhs", C.c_int64), ("hbm_bytes", C.c_int64 * 4)]
+                ("nrhs", C.c_int64), ("hbm_bytes", C.c_int64 * 4), ("graph_replays", C.c_int64)]
 
 
 class FdhError(RuntimeError):

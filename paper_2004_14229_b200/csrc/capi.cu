@@ -105,9 +105,18 @@ struct fdh_op {
   bool applied = false;
   int rank = 0, world = 1;
   int R = 1;  // right-hand sides per apply (rhs-major vectors)
+  // the apply as one CUDA graph (captured on first use for a given (x, y, stream),
+  // replayed after; the per-phase timing mode launches directly)
+  bool graphs = true, graph_failed = false;
+  cudaGraphExec_t gexec = nullptr;
+  const void* gx = nullptr;
+  const void* gy = nullptr;
+  cudaStream_t gst = nullptr;
+  int64_t graph_replays = 0;
 
   ~fdh_op() {
     if (st) cudaStreamSynchronize(st);
+    if (gexec) cudaGraphExecDestroy(gexec);
     for (void* p : allocs) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -155,6 +164,7 @@ void setup_device(fdh_op* o) {
   CK(cudaStreamCreateWithFlags(&o->st, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&o->st2, cudaStreamNonBlocking));
   if (const char* e = std::getenv("FDH_OVERLAP_NEARFIELD")) o->overlap_nf = e[0] == '1';
+  if (const char* e = std::getenv("FDH_CUDA_GRAPH")) o->graphs = e[0] != '0';
   CK(cudaDeviceGetAttribute(&o->nsm, cudaDevAttrMultiProcessorCount, o->device));
   if (const char* e = std::getenv("FDH_NF_CTAS")) o->nf_ctas = std::max(1, std::atoi(e));  // tuning knob
   CK(cudaEventCreateWithFlags(&o->ev_q, cudaEventDisableTiming));
@@ -393,13 +403,13 @@ void rec(fdh_op* o, int ph, cudaStream_t st) {
 // R right-hand sides x and y hold R vectors each, rhs-major.  The M2L runs once
 // for all of them (tile columns are (slot, rhs) pairs), the near field forms
 // every kernel value once for up to 8 of them, the other passes run per rhs.
-void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
+void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool outer_events = true) {
   Plan& P = o->P;
   const int n = P.n, np = P.n_pad;
   const int R = o->R;
   const int64_t mstr = P.S.nslots * 2 * (int64_t)np, lstr = P.T.nslots * 2 * (int64_t)np;
   int64_t L = 0;
-  CK(cudaEventRecord(o->ev_all[0], st));
+  if (outer_events) CK(cudaEventRecord(o->ev_all[0], st));  // (graph replays record them around the launch)
   rec(o, FDH_PHASE_H2D, st);
   CK(cudaMemsetAsync(o->flag, 0, sizeof(int), st));
   for (int r = 0; r < R; ++r)
@@ -557,11 +567,55 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
   for (int r = 0; r < R; ++r) launch_scatter_y(st, o->nt, o->perm_t, o->yslot + r * o->nt, y + r * o->nt);
   L += R;
   rec(o, FDH_NPHASES, st);
-  CK(cudaEventRecord(o->ev_all[1], st));
+  if (outer_events) CK(cudaEventRecord(o->ev_all[1], st));
   CK(cudaGetLastError());
   o->launches = L;
   o->applied = true;
   if (o->timing) ++o->ring_n;
+}
+
+// apply_device through a CUDA graph: ~10-20 kernel launches + memsets per apply
+// become one graph launch (capture in relaxed mode: cudaFuncSetAttribute is
+// called inside).  Any capture / instantiate failure disables graphs for the
+// operator and the apply runs directly.
+void apply_graph(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
+  if (o->timing || !o->graphs || o->graph_failed) {
+    apply_device(o, x, y, st);
+    return;
+  }
+  if (!(o->gexec && o->gx == x && o->gy == y && o->gst == st)) {
+    if (o->gexec) {
+      CK(cudaGraphExecDestroy(o->gexec));
+      o->gexec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      try {
+        apply_device(o, x, y, st, false);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok && g != nullptr;
+    }
+    if (ok) ok = cudaGraphInstantiate(&o->gexec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+      (void)cudaGetLastError();
+      o->gexec = nullptr;
+      o->graph_failed = true;
+      apply_device(o, x, y, st);
+      return;
+    }
+    o->gx = x;
+    o->gy = y;
+    o->gst = st;
+  }
+  CK(cudaEventRecord(o->ev_all[0], st));
+  CK(cudaGraphLaunch(o->gexec, st));
+  CK(cudaEventRecord(o->ev_all[1], st));
+  o->applied = true;
+  ++o->graph_replays;
 }
 
 void collect_times(fdh_op* o) {
@@ -743,7 +797,7 @@ int fdh_apply_multi(fdh_op* o, const double* x, int64_t k, double* y) {
         CK(cudaMemsetAsync(o->xin + nb * o->ns, 0, sizeof(double2) * (size_t)((R - nb) * o->ns), o->st));
       CK(cudaMemcpyAsync(o->xin, x + 2 * b * o->ns, sizeof(double2) * (size_t)(nb * o->ns), cudaMemcpyHostToDevice,
                          o->st));
-      apply_device(o, o->xin, o->yout, o->st);
+      apply_graph(o, o->xin, o->yout, o->st);
       CK(cudaMemcpyAsync(y + 2 * b * o->nt, o->yout, sizeof(double2) * (size_t)(nb * o->nt),
                          cudaMemcpyDeviceToHost, o->st));
       int flag = 0;
@@ -763,7 +817,7 @@ int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream
   if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
   return guard([&] {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : o->st;
-    apply_device(o, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), st);
+    apply_graph(o, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), st);
   });
 }
 
@@ -817,6 +871,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->w_resident = o->w_resident ? 1 : 0;
   s->w_segments = (int64_t)o->segs.size();
   s->nrhs = o->R;
+  s->graph_replays = o->graph_replays;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

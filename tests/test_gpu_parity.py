@@ -261,3 +261,19 @@ def test_onthefly_coupling_segments_int8(m, monkeypatch):
     assert st["m2l_impl"] == 1 and st["w_resident"] == 0 and st["w_segments"] >= 2
     y = op.apply(q)
     assert np.array_equal(y, y_res)  # same digits and scales, same summation order
+
+
+def test_cuda_graph_replay_matches_direct(monkeypatch):
+    """The apply runs as a replay of a captured CUDA graph (one graph launch per
+    apply); the direct launches (FDH_CUDA_GRAPH=0) give the same bits."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
+    op = F.DirectionalOperator(*args)
+    y1 = op.apply(q)
+    y2 = op.apply(2 * q)
+    assert op.stats()["graph_replays"] >= 2
+    monkeypatch.setenv("FDH_CUDA_GRAPH", "0")
+    opd = F.DirectionalOperator(*args)
+    assert np.array_equal(opd.apply(q), y1) and np.array_equal(opd.apply(2 * q), y2)
+    assert opd.stats()["graph_replays"] == 0
