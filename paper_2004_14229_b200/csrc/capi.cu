@@ -747,7 +747,7 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
 extern "C" {
 
 const char* fdh_last_error(void) { return g_err.c_str(); }
-const char* fdh_version(void) { return "fdhelm-b200 0.1 (sm_100a, FP64 DMMA M2L)"; }
+const char* fdh_version(void) { return "fdhelm-b200 0.2 (sm_100a; M2L: tcgen05 int8 digit products, FP64 DMMA selectable)"; }
 
 int fdh_create(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx, const double* sy,
                const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3], double kappa, int n_max,
