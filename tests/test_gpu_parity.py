@@ -277,3 +277,14 @@ def test_cuda_graph_replay_matches_direct(monkeypatch):
     opd = F.DirectionalOperator(*args)
     assert np.array_equal(opd.apply(q), y1) and np.array_equal(opd.apply(2 * q), y2)
     assert opd.stats()["graph_replays"] == 0
+
+
+def test_overlapped_near_field_same_bits(monkeypatch):
+    """FDH_OVERLAP_NEARFIELD=1: the near field as a persistent grid on the second
+    stream, launched before the M2L -- same y bits as the sequential order."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
+    y = F.DirectionalOperator(*args).apply(q)
+    monkeypatch.setenv("FDH_OVERLAP_NEARFIELD", "1")
+    assert np.array_equal(F.DirectionalOperator(*args).apply(q), y)
