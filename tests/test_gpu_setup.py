@@ -89,3 +89,19 @@ def test_gpu_structure_chunked_pairs(monkeypatch):
     c = CONFIGS[2]
     tg, sr, _ = make_inputs(c, nt=40000, ns=30000)
     compare(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+
+
+@pytest.mark.parametrize("name", ["uniform", "snapped", "grid_k3"])
+def test_gpu_tree_golden(name):
+    """Trees built on the B200 (k_setup.cu) against the reference's own trees
+    (tests/golden, written from oracle/_ref by tools/make_golden.py)."""
+    import os
+
+    G = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_r01.npz"))
+    p = G[f"tree_{name}_pts"]
+    lo, hi = G[f"tree_{name}_root"]
+    pts = [np.ascontiguousarray(p[:, a]) for a in range(3)]
+    op = F.DirectionalOperator(pts, pts, lo, hi, 1.0, n_max=int(G[f"tree_{name}_nmax"]), m=1)
+    assert op.stats()["gpu_structure"] == 1
+    assert np.array_equal(op.tree(0), G[f"tree_{name}_rows"])
+    assert np.array_equal(op.perm(0), G[f"tree_{name}_perm"])
