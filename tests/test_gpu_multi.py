@@ -87,3 +87,17 @@ def test_multi_rhs_single_apply_and_errors():
         F.DirectionalOperator(*args, nrhs=3)  # not a power of two
     with pytest.raises(F.FdhError):
         op.apply_multi(np.zeros((2, 7), dtype=np.complex128))  # dimension mismatch
+
+
+def test_multi_rhs_shards_sum_to_full():
+    """Target shards (fdh_create_multi with rank / world) of a multi-vector
+    operator: the rank outputs sum to the full multi-vector apply."""
+    c = CONFIGS[2]
+    tg, sr, _ = make_inputs(c, nt=20000, ns=15000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
+    X = _charges(4, 15000, 21)
+    full = F.DirectionalOperator(*args, nrhs=4).apply_multi(X)
+    acc = np.zeros_like(full)
+    for rank in range(2):
+        acc += F.DirectionalOperator(*args, rank=rank, world=2, nrhs=4).apply_multi(X)
+    assert oracle.rel_l2(acc, full) <= I8
