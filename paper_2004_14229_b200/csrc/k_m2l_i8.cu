@@ -40,6 +40,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef FDH_I8_BALANCED
+#define FDH_I8_BALANCED 1  // split N > 256 into equal MMAs (0: 256 + rest; tools/gpu_i8_split.sh: ~1 % on config 2)
+#endif
 #ifndef FDH_I8_EXP
 #define FDH_I8_EXP 0  // timing experiments: 1 = no B gather, 2 = no W copy, 3 = neither (wrong results)
 #endif
@@ -398,11 +401,16 @@ __global__ void __maxnreg__(128)
           const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
 #pragma unroll
           for (int b = 0; b < MB; ++b) {
+            // N > 256 splits into equal parts (multiples of 32 columns) with
+            // FDH_I8_BALANCED: e.g. 320 -> 160 + 160 rather than 256 + 64
+            const int nsp = (ncol + 255) / 256;
+            const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
 #pragma unroll
-            for (int p0 = 0; p0 < ncol; p0 += 256) {
-              const int np = ncol - p0 < 256 ? ncol - p0 : 256;
+            for (int p0 = 0; p0 < ncol;) {
+              const int np = ncol - p0 < part ? ncol - p0 : part;
               mma_i8(tmem + b * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
                      dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
+              p0 += np;
             }
           }
         }
