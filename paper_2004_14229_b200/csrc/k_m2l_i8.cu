@@ -40,6 +40,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef FDH_I8_SLEEP_NS
+#define FDH_I8_SLEEP_NS 128  // producer back-off between empty-barrier polls
+#endif
 #ifndef FDH_I8_BALANCED
 #define FDH_I8_BALANCED 1  // split N > 256 into equal MMAs (0: 256 + rest; tools/gpu_i8_split.sh: ~1 % on config 2)
 #endif
@@ -106,7 +109,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
         : "r"(smem_u32(bar)), "r"(phase)
         : "memory");
     if (ok) return;
-    __nanosleep(128);
+    __nanosleep(FDH_I8_SLEEP_NS);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
