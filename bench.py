@@ -375,7 +375,7 @@ def run_ours(args, c, rank, world, local_rank):
                 "frac_of_fp64_peak": (24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 / peak
                                       if (p2p_ms > 0 and peak) else None),
                 "note": "24 flop per pair (SURVEY.md 8(d), rsqrt and sincos counted as 1 each); the kernel issues "
-                        "~35 FP64 instructions per pair (SASS), FP64 pipe ~67 % active (profiles/r01_ncu_p2p_fast.json)"},
+                        "~33 FP64 instructions per pair (SASS), FP64 pipe 64 % active (profiles/r01_ncu_p2p_unroll4.json)"},
         "hbm_passes": hbm_passes(st, ph),
         "counters": {k: st[k] for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s",
                                         "depth_t", "depth_s")},
