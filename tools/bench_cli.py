@@ -124,7 +124,7 @@ def main(argv=None) -> int:
             "nf_percent": st["nf_percent"], "N_SC": st["n_sc"], "N_C": st["n_c"], "N_LE": st["n_le"],
             "M_D": st["m_d"], "bytes_stored": st["bytes_stored"],
             "sampled_rel_error": oracle.rel_l2(y[rows], yd), "sample_rows": int(len(rows)),
-            "hardware": "1x NVIDIA B200 (fdhelm-b200, FP64 DMMA)", "no_aca": True,
+            "hardware": "1x NVIDIA B200 (fdhelm-b200, M2L: " + ("int8 tcgen05 digit products" if st["m2l_impl"] == 1 else "FP64 DMMA") + ")", "no_aca": True,
         }
         if not a.points and a.k in PAPER_TABLE1:
             p = PAPER_TABLE1[a.k]
