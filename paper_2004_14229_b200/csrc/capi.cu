@@ -47,6 +47,7 @@ struct fdh_op {
   // trees (slot order)
   double *tx = nullptr, *ty = nullptr, *tz = nullptr, *sx = nullptr, *sy = nullptr, *sz = nullptr;
   uint32_t *perm_t = nullptr, *perm_s = nullptr;
+  uint32_t* diag_slot = nullptr;  // zero diagonal: source slot of each target's original index
   int32_t* tslot_dir = nullptr;
   // S2M
   int n_s2m = 0;
@@ -216,6 +217,15 @@ void setup_device(fdh_op* o) {
   o->sz = o->up(P.S.z);
   o->perm_t = o->up(P.T.perm);
   o->perm_s = o->up(P.S.perm);
+  if (P.prm.zero_diagonal) {
+    // zero diagonal: per target slot the source slot holding the same
+    // original index (~0u if none), so the near field compares slot numbers
+    std::vector<uint32_t> inv(P.S.perm.size()), dslot(P.T.perm.size(), ~0u);
+    for (size_t k = 0; k < P.S.perm.size(); ++k) inv[P.S.perm[k]] = (uint32_t)k;
+    for (size_t j = 0; j < P.T.perm.size(); ++j)
+      if (P.T.perm[j] < P.S.perm.size()) dslot[j] = inv[P.T.perm[j]];
+    o->diag_slot = o->up(dslot);
+  }
   o->tslot_dir = o->up(P.T.slot_dir);
   // S2M
   o->n_s2m = (int)P.s2m_slot.size();
@@ -437,7 +447,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   auto near_field = [&](cudaStream_t snf, int grid) {
     if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
     launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
-               o->tz, o->sx, o->sy, o->sz, o->q4, o->perm_t, o->perm_s, P.prm.zero_diagonal, o->ynear, o->flag,
+               o->tz, o->sx, o->sy, o->sz, o->q4, o->diag_slot, nullptr, P.prm.zero_diagonal, o->ynear, o->flag,
                o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt, grid);
     L += (o->n_leaf > 0) * p2p_launches(R);
     if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
