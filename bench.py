@@ -2,15 +2,23 @@
 """Benchmark of the directional Helmholtz matvec (BASELINE.json metric:
 "directional-FMM matvec time & (N_T+N_S)/s at 1/2/4/8 B200; % FP64 roofline").
 
-A step = one apply y = A x of the configured workload (default: BASELINE config
-2, N_T = N_S = 100,000, kappa = 16, m = 4, the config the metric is quoted on
-that fits one GPU).  Setup (trees, partition, coupling matrices) is outside the
-timed region, as t_s in PAPER.md Table 1.
+A step = one apply y = A x of the configured workload.  Default: BASELINE
+config 4 (N_T = N_S = 4,000,000, kappa = 64, m = 6) -- the scaling config the
+metric is quoted on ("at 1/2/4/8 B200"), the largest that runs on one GPU.
+Setup (trees, partition, coupling scales) is outside the timed region, as t_s in
+PAPER.md Table 1, and reported as config.setup_s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank owns a cost-balanced Morton range of target
-leaves (fdh_create_shard) and the step ends with an NCCL all-reduce of y.
+Timed region (every step, N = 1): the C-ABI host call fdh_apply with pinned host
+buffers (H2D of x, the apply as one CUDA-graph replay, D2H of y) -- `e2e` -- and,
+inside it, the device time of the apply kernels from the library's CUDA events
+around the graph launch -- `value` (inputs already in HBM).  The per-phase times
+and the M2L kernel time come from event-record nodes inside the same replays.
+N > 1 (torchrun, or `--gpus N` which re-launches itself under torchrun): every
+rank owns a cost-balanced Morton range of target leaves (fdh_create_shard) and
+the step is H2D + fdh_apply_device + NCCL all-reduce of y + D2H on the
+operator's stream; times are the max over ranks.
 `--impl reference` times the CPU restatement of the reference algorithm
 (oracle/, OpenMP, all host cores) on a bounded sample of the same workload.
 """
@@ -19,6 +27,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -49,8 +58,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=0.2):
         self.index = index
+        self.period = period
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -64,7 +74,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -86,78 +96,117 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_oracle(c, tg, sr):
-    import oracle
+# ---------------------------------------------------------------- CPU reference
+class CpuReference:
+    """The CPU restatement of the reference algorithm (oracle/, TEST INFRASTRUCTURE,
+    OpenMP over all host threads) on bounded samples of the workload.
 
-    return oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf, c.depth_cap,
-                         c.zero_diagonal)
+    The sampled-structure oracle (orc_create_sampled) builds both trees in full and
+    refines the partition below the sampled target leaves' ancestors; each sample
+    is a set of COMPLETE sibling groups (all leaf children of random parent boxes)
+    so the parent level's M2L is paid once per 8 leaves, as in a full run.  Per
+    sample the oracle reports its upward-pass, coupling-generation (once per key
+    the sample uses), M2L and downward/near-field seconds; the full apply is
+    extrapolated as upward + coupling x N_SC / keys used + (M2L + downward) x
+    target leaves / sampled leaves (label: extrapolated)."""
 
+    def __init__(self, c, tg, sr, nsamples, groups_per_sample=1, seed=7):
+        import oracle
 
-def cpu_oracle_sample(c, tg, sr, q, target_s=12.0, o=None, seed=7, single_core=True):
-    """The CPU restatement (oracle/) on a bounded sample: full upward pass plus
-    M2L/L2L/L2T/P2P for a seeded sample of target leaves; the full-apply time is
-    extrapolated linearly in the number of target leaves."""
-    import oracle
-
-    cores = oracle.lib().orc_set_threads(0)
-    if o is None:
-        o = build_oracle(c, tg, sr)
-    nl = o.leaf_count(0)
-    rng = np.random.default_rng(seed)
-    t = time.perf_counter()
-    o.apply_sampled(q, np.zeros(0, dtype=np.int64))
-    t0 = time.perf_counter() - t
-    k = min(nl, 16)
-    t = time.perf_counter()
-    o.apply_sampled(q, rng.choice(nl, k, replace=False))
-    tk = time.perf_counter() - t
-    per_leaf = max((tk - t0) / k, 1e-9)
-    k2 = int(min(nl, max(k, (target_s - t0) / per_leaf)))
-    t = time.perf_counter()
-    o.apply_sampled(q, rng.choice(nl, k2, replace=False))
-    tk2 = time.perf_counter() - t
-    t_full = t0 + (tk2 - t0) * nl / k2
-    # the same restatement on ONE core (SURVEY.md 8(d): nproc cores and 1 core), a
-    # smaller leaf sample (~1/4 of the budget), extrapolated the same way
-    if not single_core:
-        return {"value": (c.nt + c.ns) / t_full, "unit": UNIT, "cores": int(cores), "kind": "port",
-                "sample": (f"oracle/ (CPU restatement, OpenMP {cores} threads): full S2M+M2M, then M2L/L2L/L2T/P2P "
-                           f"for {k2} of {nl} seeded target leaves in {tk2:.2f} s; full apply extrapolated to "
-                           f"{t_full:.2f} s (linear in target leaves; upward pass {t0:.2f} s)"),
-                "seconds_measured": tk2, "apply_s_extrapolated": t_full}
-    L = oracle.lib()
-    L.orc_set_threads(1)
-    try:
+        self.oracle = oracle
+        self.c = c
+        self.cores = int(oracle.lib().orc_set_threads(0))
+        args = (tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf, c.depth_cap, c.zero_diagonal)
         t = time.perf_counter()
-        o.apply_sampled(q, np.zeros(0, dtype=np.int64))
-        s0 = time.perf_counter() - t
-        k1 = int(min(nl, max(2, (target_s / 4 - s0) / max(per_leaf * cores, 1e-9))))
+        probe = oracle.Oracle(*args, sample_leaves=[0])
+        tt = probe.tree(0)
+        self.n_sc = None
+        del probe
+        lv = tt[tt[:, 6] == 1]
+        self.nl = len(lv)
+        # parent of each leaf = its coordinate >> 1 at level - 1
+        par = np.stack([lv[:, 0] - 1, lv[:, 1] >> 1, lv[:, 2] >> 1, lv[:, 3] >> 1], axis=1)
+        _, gid = np.unique(par, axis=0, return_inverse=True)
+        gid = gid.reshape(-1)
+        ngroups = int(gid.max()) + 1
+        rng = np.random.default_rng(seed)
+        pick = rng.choice(ngroups, min(ngroups, nsamples * groups_per_sample), replace=False)
+        self.samples = []
+        for i in range(nsamples):
+            gsel = pick[i * groups_per_sample:(i + 1) * groups_per_sample]
+            self.samples.append(np.nonzero(np.isin(gid, gsel))[0].astype(np.int64))
+        allv = np.unique(np.concatenate(self.samples))
+        self.op = oracle.Oracle(*args, sample_leaves=allv)
+        self.setup_s = time.perf_counter() - t
+        self.q = None
+
+    def run(self, q, i, n_sc):
         t = time.perf_counter()
-        o.apply_sampled(q, rng.choice(nl, k1, replace=False))
-        sk = time.perf_counter() - t
-    finally:
-        L.orc_set_threads(int(cores))
-    t1 = s0 + (sk - s0) * nl / k1
-    single = {"value": (c.nt + c.ns) / t1, "unit": UNIT, "cores": 1, "apply_s_extrapolated": t1,
-              "sample": f"same restatement, 1 thread: {k1} of {nl} target leaves in {sk:.2f} s (upward pass {s0:.2f} s)"}
-    return {
-        "value": (c.nt + c.ns) / t_full,
-        "unit": UNIT,
-        "cores": int(cores),
-        "kind": "port",
-        "sample": (f"oracle/ (CPU restatement, OpenMP {cores} threads): full S2M+M2M, then M2L/L2L/L2T/P2P for "
-                   f"{k2} of {nl} seeded target leaves in {tk2:.2f} s; full apply extrapolated to {t_full:.2f} s "
-                   f"(linear in target leaves; upward pass {t0:.2f} s)"),
-        "seconds_measured": tk2,
-        "apply_s_extrapolated": t_full,
-        "single_core": single,
+        self.op.apply_sampled(q, self.samples[i])
+        wall = time.perf_counter() - t
+        tm = self.op.last_timing()
+        k = max(tm["keys_generated"], 1.0)
+        full = (tm["upward"] + tm["coupling"] * n_sc / k + (tm["m2l"] + tm["down_nf"]) * self.nl / len(self.samples[i]))
+        return {"wall_s": wall, "apply_s_extrapolated": full, "timing": tm, "leaves": int(len(self.samples[i]))}
+
+    def describe(self, r, n):
+        tm = r["timing"]
+        return (f"oracle/ (CPU restatement of PAPER Alg. 4, OpenMP {self.cores} threads), sampled-structure mode: "
+                f"{n} sample(s) of complete sibling groups of target leaves (last: {r['leaves']} of {self.nl} leaves, "
+                f"{r['wall_s']:.1f} s: upward {tm['upward']:.2f} s, coupling generation {tm['coupling']:.2f} s for "
+                f"{int(tm['keys_generated'])} keys, M2L {tm['m2l']:.2f} s, L2L/L2T/near field {tm['down_nf']:.2f} s); "
+                f"full apply extrapolated to {r['apply_s_extrapolated']:.1f} s = upward + coupling x N_SC / keys + "
+                f"(M2L + downward) x leaves ratio")
+
+
+def run_reference(args, c, rank, world):
+    """--impl reference: the reference algorithm on the host cores (oracle port)."""
+    if rank != 0:
+        return
+    tg, sr, q = make_inputs(c)
+    n_sc = int(json.load(open(os.path.join(ROOT, "tests", "golden", f"structure_cfg{c.cfg}.json")))["counts"]["n_sc"])
+    ref = CpuReference(c, tg, sr, args.steps, groups_per_sample=args.ref_groups)
+    for _ in range(args.warmup):  # warm-up: the upward pass only (no target leaves)
+        ref.op.apply_sampled(q, np.zeros(0, dtype=np.int64))
+    steps = []
+    r = None
+    for i in range(args.steps):
+        r = ref.run(q, i, n_sc)
+        steps.append(r["apply_s_extrapolated"])
+    t = float(np.mean(steps))
+    value = (c.nt + c.ns) / t
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic (seeded, SURVEY.md 8(d))",
+        "config": {"workload": workload_desc(c), "cfg": c.cfg},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
+                         "sample": ref.describe(r, args.steps) + f"; mean over {args.steps} samples (extrapolated)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": ref.setup_s,
     }
+    print(json.dumps(out), flush=True)
 
 
-def roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traffic):
+def cpu_baseline(c, tg, sr, q, seconds):
+    """cpu_baseline leg of our arm (rank 0, N = 1): one or two sibling-group samples."""
+    n_sc = int(json.load(open(os.path.join(ROOT, "tests", "golden", f"structure_cfg{c.cfg}.json")))["counts"]["n_sc"])
+    ref = CpuReference(c, tg, sr, 2, groups_per_sample=1, seed=11)
+    r1 = ref.run(q, 0, n_sc)
+    rs = [r1]
+    if r1["wall_s"] < 0.5 * seconds:
+        rs.append(ref.run(q, 1, n_sc))
+    t = float(np.mean([r["apply_s_extrapolated"] for r in rs]))
+    return {"value": (c.nt + c.ns) / t, "unit": UNIT, "cores": ref.cores, "kind": "port",
+            "sample": ref.describe(rs[-1], len(rs)) + f"; mean of {len(rs)} (extrapolated)"}
+
+
+# ---------------------------------------------------------------- roofline
+def roofline_block(st, c, m2l_flops, peak, gemm_ms, ms_per_step, traffic):
     """Roofline of the M2L kernel: the int8 tcgen05 digit GEMM (k_m2l_i8) against
     the measured int8 tensor peak, or the FP64 DMMA GEMM against the FP64 peak."""
     share = gemm_ms / ms_per_step if ms_per_step else None
+    achieved = m2l_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     fp64 = {"achieved_tflops": achieved, "fp64_peak_tflops": peak,
             "ratio": (achieved / peak) if (achieved and peak) else None,
             "note": "algorithmic FP64 flop (8 n^2 per admissible block) per second of the M2L kernel, against the "
@@ -175,27 +224,22 @@ def roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traff
                 "achieved": ach, "peak": tops, "unit": "TOPS", "frac": (ach / tops) if (ach and tops) else None,
                 "traffic": traffic,
                 "peak_source": "measured live: fdh_tensor_peak_tops(0) int8 tcgen05 microbenchmark, M=128 N=256 "
-                               "(MEASURED_PEAKS.json has no int8 entry; its bf16 burst 1625.8 TF/s x 2 = 3252 for "
-                               "comparison)",
+                               "(MEASURED_PEAKS.json has no int8 entry; 2 x its bf16 burst for comparison)",
                 "algorithmic": f"28 digit products x 8 n^2 ops per admissible block x N_C={st['n_c']} = {alg:.4g} "
-                               f"int8 ops per launch",
+                               f"int8 ops per apply",
                 "issued_ops": st["m2l_i8_ops"], "issued_frac": (iss / tops) if (iss and tops) else None,
                 "issued_note": "int8 ops the kernel issues: every target column of a tile for every key of the tile "
                                "(absent columns are zero), rows padded to 128, K to 2 x 16k",
-                "fp64_equivalent": fp64, "gemm_ms": gemm_ms, "share_of_step": share}
+                "fp64_equivalent": fp64, "gemm_ms": gemm_ms, "share_of_step": share,
+                "timing": "CUDA event-record nodes inside the timed graph replays, on the operator's stream"}
     return {"bound": "tensor", "kernel": "k_m2l_gemm (FP64 DMMA mma.sync.m8n8k4)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
             "peak_source": "measured live: fdh_fp64_peak_tflops(0) DMMA microbenchmark (no FP64 entry in "
                            "MEASURED_PEAKS.json)",
             "algorithmic": f"8 n^2 flop per admissible block x N_C={st['n_c']} = {m2l_flops:.4g} flop per "
-                           f"launch (SURVEY.md 8(d); the count holds for a 3M complex product)",
-            "issued_flop": st["m2l_flops_executed"],
-            "issued_frac": (st["m2l_flops_executed"] / (gemm_ms * 1e-3) / 1e12 / peak
-                            if (gemm_ms > 0 and peak) else None),
-            "issued_note": "flop the kernel issues on DMMA: Gauss 3-multiplication product (6 n^2) for "
-                           "8-target n-tiles, 8 n^2 real GEMM for <= 4, incl. padding columns",
-            "gemm_ms": gemm_ms, "share_of_step": share}
+                           f"apply (SURVEY.md 8(d); the count holds for a 3M complex product)",
+            "issued_flop": st["m2l_flops_executed"], "gemm_ms": gemm_ms, "share_of_step": share}
 
 
 def hbm_passes(st, ph):
@@ -207,9 +251,7 @@ def hbm_passes(st, ph):
         src = "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
         peak, src = 7700.0, "fallback: nominal B200 HBM3e (MEASURED_PEAKS.json absent)"
-    out = {"peak_gbs": peak, "peak_source": src,
-           "note": "< 1 % of the step; per (box, direction) work items of 15-60 points are latency / FP64-bound "
-                   "(sincos, Lagrange cardinals per point), not bandwidth-bound, at these sizes"}
+    out = {"peak_gbs": peak, "peak_source": src}
     for k in ("s2m", "m2m", "l2l", "l2t"):
         b, ms = st["hbm_bytes"][k], ph.get(k, 0.0)
         gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else None
@@ -217,34 +259,7 @@ def hbm_passes(st, ph):
     return out
 
 
-def run_reference(args, c, rank, world):
-    """--impl reference: the reference algorithm on the host cores (oracle port)."""
-    if rank != 0:
-        return
-    tg, sr, q = make_inputs(c)
-    steps = []
-    cb = None
-    o = build_oracle(c, tg, sr)
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(c, tg, sr, q, target_s=args.ref_seconds, o=o, seed=7 + i, single_core=False)
-        if i >= args.warmup:
-            steps.append(r["apply_s_extrapolated"])
-            cb = r
-    t = float(np.mean(steps))
-    value = (c.nt + c.ns) / t
-    cb = dict(cb)
-    cb["value"] = value
-    out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic (seeded, SURVEY.md 8(d))",
-        "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": "cpu-openmp"},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(out), flush=True)
-
-
+# ---------------------------------------------------------------- our arm
 def run_ours(args, c, rank, world, local_rank):
     import torch
 
@@ -261,86 +276,71 @@ def run_ours(args, c, rank, world, local_rank):
     op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf, c.depth_cap,
                                c.zero_diagonal, rank=rank, world=world)
     setup_s = time.perf_counter() - t_setup
-    st0 = op.stats()
     stream = torch.cuda.ExternalStream(op.stream(), device=dev)
-    x = torch.from_numpy(q.view(np.float64)).to(dev)
+    xh_t = torch.from_numpy(q.view(np.float64).copy()).pin_memory()
+    yh_t = torch.empty(2 * c.nt, dtype=torch.float64).pin_memory()
+    xh, yh = xh_t.numpy().view(np.complex128), yh_t.numpy().view(np.complex128)
+    x = torch.empty(2 * c.ns, dtype=torch.float64, device=dev)
     y = torch.empty(2 * c.nt, dtype=torch.float64, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
-    torch.cuda.synchronize()  # x / y are produced on torch's stream, consumed on the operator's
+    torch.cuda.synchronize()
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
     def step():
+        """one e2e step; returns the device ms of the apply alone (N > 1: events
+        around fdh_apply_device on the operator's stream)"""
+        if world == 1:
+            op.apply(xh, out=yh)  # C-ABI host call: H2D, graph replay, D2H, sync
+            return None
+        with torch.cuda.stream(stream):
+            x.copy_(xh_t, non_blocking=True)
+            ev_a[0].record(stream)
         op.apply_device(x.data_ptr(), y.data_ptr(), op.stream())
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(y)
+        with torch.cuda.stream(stream):
+            ev_a[1].record(stream)
+            dist.all_reduce(y)
+            yh_t.copy_(y, non_blocking=True)
+        stream.synchronize()
+        return ev_a[0].elapsed_time(ev_a[1])
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    op.sync()  # deferred device errors of the warm-up (fdh_sync)
     if world > 1:
         dist.barrier()
+    op.set_timing(True)  # phase events as event-record nodes inside the graph replays
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    op.set_timing(True)
+    dev_ms = []
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(local_rank, period=0.2 if args.config <= 2 else 1.0) as clk:
         for i in range(args.steps):
             with torch.cuda.stream(stream):
-                flush.zero_()  # L2 flush between timed steps (outside the events)
+                flush.zero_()  # L2 flush between timed steps (outside the step events)
                 evs[i][0].record(stream)
-            step()
+            d = step()
             evs[i][1].record(stream)
+            if d is not None:
+                dev_ms.append(d)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    op.sync()
     st = op.stats()
-    op.set_timing(False)
+    e2e_ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world == 1:
+        assert st["applies_collected"] == args.steps, st["applies_collected"]
+        apply_ms = st["apply_ms_sum"]
+    else:
+        apply_ms = sum(dev_ms)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([apply_ms, e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = args.steps * (c.nt + c.ns) / (total_ms / 1e3)
-
-    # ---- e2e: host buffers (pinned), copies inside the timed region.  N = 1: the
-    # C-ABI host call fdh_apply; N > 1: H2D + fdh_apply_device + NCCL all-reduce
-    # of the rank partials + D2H, all on the operator's stream.
-    xh_t = torch.from_numpy(q.copy()).pin_memory()
-    yh_t = torch.empty(c.nt, dtype=torch.complex128).pin_memory()
-    xh, yh = xh_t.numpy(), yh_t.numpy()
-
-    def e2e_step():
-        if world == 1:
-            op.apply(xh, out=yh)
-        else:
-            with torch.cuda.stream(stream):
-                x.copy_(xh_t.view(torch.float64), non_blocking=True)
-            op.apply_device(x.data_ptr(), y.data_ptr(), op.stream())
-            with torch.cuda.stream(stream):
-                dist.all_reduce(y)
-                yh_t.view(torch.float64).copy_(y, non_blocking=True)
-            stream.synchronize()
-
-    e2e_step()  # warm the host path (pinned buffers, copy engines)
-    torch.cuda.synchronize()
-    if world > 1:
+        apply_ms, e2e_ms = float(t[0].item()), float(t[1].item())
         dist.barrier()
-    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_s.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e_e.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e_s.elapsed_time(e_e)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-        dist.barrier()
+    ms_per_step = apply_ms / args.steps
+    value = args.steps * (c.nt + c.ns) / (apply_ms / 1e3)
     e2e_value = args.steps * (c.nt + c.ns) / (e2e_ms / 1e3)
-
     if rank != 0:
         return
     # ---- roofline of the dominant kernel (the M2L GEMM)
@@ -348,12 +348,10 @@ def run_ours(args, c, rank, world, local_rank):
     n = (c.m + 1) ** 3
     m2l_flops = 8.0 * n * n * st["n_c"]  # algorithmic
     gemm_ms = st["m2l_gemm_ms"]
-    achieved = m2l_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
     traffic = None
     if os.path.exists(PROFILE_TRAFFIC):
         try:
-            tr = json.load(open(PROFILE_TRAFFIC))
-            traffic = tr.get(f"cfg{c.cfg}{'_i8' if st['m2l_impl'] == 1 else ''}")
+            traffic = json.load(open(PROFILE_TRAFFIC)).get(f"cfg{c.cfg}{'_i8' if st['m2l_impl'] == 1 else ''}")
         except Exception:
             traffic = None
     ph = st["phase_ms"]
@@ -366,57 +364,69 @@ def run_ours(args, c, rank, world, local_rank):
                   "on tcgen05)" if st["m2l_impl"] == 1 else "complex128 (f64)"),
         "data": "synthetic (seeded uniform / Gaussian-mixture points, U(-1,1) complex charges; SURVEY.md 8(d))",
         "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": f"target-leaf shards x{world}",
-                   "l2": "flushed between timed steps (256 MB write, outside the step events)",
+                   "l2": "flushed between timed steps (256 MB write, outside the step events); the apply's working "
+                         "set (coupling digits, moments) is far larger than L2",
+                   "launch_mode": f"CUDA graph replays ({st['graph_replays']} in total incl. warm-up), phase timing "
+                                  f"by event-record nodes inside the graph",
                    "setup_s": setup_s},
-        "roofline": roofline_block(st, c, m2l_flops, achieved, peak, gemm_ms, ms_per_step, traffic),
+        "roofline": roofline_block(st, c, m2l_flops, peak, gemm_ms, ms_per_step, traffic),
         "phases_ms": ph,
         "p2p": {"pairs": st["m_d"], "ms": p2p_ms,
                 "tflops_24flop_per_pair": 24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 if p2p_ms > 0 else None,
                 "frac_of_fp64_peak": (24.0 * st["m_d"] / (p2p_ms * 1e-3) / 1e12 / peak
                                       if (p2p_ms > 0 and peak) else None),
-                "note": "24 flop per pair (SURVEY.md 8(d), rsqrt and sincos counted as 1 each); the kernel issues "
-                        "~33 FP64 instructions per pair (SASS), FP64 pipe 64 % active (profiles/r01_ncu_p2p_unroll4.json)"},
+                "note": "24 flop per pair (SURVEY.md 8(d), rsqrt and sincos counted as 1 each)"},
         "hbm_passes": hbm_passes(st, ph),
         "counters": {k: st[k] for k in ("n_c", "n_sc", "m_d", "n_le", "n_lminus", "l_hf", "slots_t", "slots_s",
                                         "depth_t", "depth_s")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * c.ns, "d2h_bytes_per_step": 16 * c.nt,
                 "ms_per_step": e2e_ms / args.steps,
-                "path": ("fdh_apply (C-ABI) with pinned host buffers" if world == 1 else
-                         "pinned H2D + fdh_apply_device + NCCL all-reduce of y + D2H")},
+                "path": ("fdh_apply (C-ABI host call) with pinned host buffers, the same applies as `value`"
+                         if world == 1 else "pinned H2D + fdh_apply_device + NCCL all-reduce of y + D2H")},
         "gpu_launches": int(st["gpu_launches"]) * args.steps,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = {k: v for k, v in cpu_oracle_sample(c, tg, sr, q, args.cpu_seconds).items()
-                                   if k in ("value", "unit", "cores", "kind", "sample", "single_core")}
+            out["cpu_baseline"] = cpu_baseline(c, tg, sr, q, args.cpu_seconds)
         except Exception as e:  # the baseline is reported, never required
             out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
     print(json.dumps(out), flush=True)
-    del st0
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--ref-groups", type=int, default=1, help="sibling groups of target leaves per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the line)
+        env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.run(cmd, env=env).returncode)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     c = CONFIGS[args.config]
     if args.impl == "reference":
         if rank == 0:
-            # every step is a bounded sample; keep the whole run within a few minutes
-            args.ref_seconds = max(1.0, min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup)))
             subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=False)
         run_reference(args, c, rank, world)
         return
@@ -424,6 +434,11 @@ def main():
         import torch
         import torch.distributed as dist
 
+        if torch.cuda.device_count() < world:
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "error": f"--gpus {world} needs {world} visible GPUs, "
+                                                              f"found {torch.cuda.device_count()}"}), flush=True)
+            sys.exit(1)
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     run_ours(args, c, rank, world, local_rank)

@@ -91,6 +91,9 @@ typedef struct fdh_stats {
   int64_t nrhs;                 /* right-hand sides per device apply (fdh_create_multi)    */
   int64_t hbm_bytes[4];         /* algorithmic HBM bytes per rhs of S2M, M2M, L2L, L2T     */
   int64_t graph_replays;        /* applies run as a replay of the captured CUDA graph      */
+  double apply_ms_sum;          /* sum of apply_ms over the applies collected since the
+                                   last fdh_set_timing (host-path applies: every one)      */
+  int64_t applies_collected;
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table
@@ -141,13 +144,20 @@ int fdh_apply(fdh_op* op, const double* x, double* y);
 int fdh_apply_multi(fdh_op* op, const double* x, int64_t k, double* y);
 /* Device-resident variant: x_dev / y_dev are device pointers (complex128,
  * original order); enqueued on `stream` (cudaStream_t, NULL = the operator's
- * own stream) and not synchronised. */
+ * own stream) and not synchronised.  Errors detected on the device (singular
+ * kernel -> FDH_ERR_DOMAIN, as the reference's domain_error) are DEFERRED: they
+ * accumulate over device-path applies and are returned by fdh_sync. */
 int fdh_apply_device(fdh_op* op, const double* x_dev, double* y_dev, void* stream);
+/* Wait for the operator's applies and return (and clear) the deferred device
+ * error of the fdh_apply_device calls since the last fdh_sync. */
+int fdh_sync(fdh_op* op);
 /* The operator's stream (cudaStream_t) for event timing by the caller. */
 void* fdh_stream(fdh_op* op);
 /* Enable per-phase CUDA-event timing (events recorded between the phases of
- * every apply on its stream; fdh_get_stats averages the applies recorded since
- * this call, up to the last 64).  Resets the average. */
+ * every apply on its stream -- inside the CUDA graph as event-record nodes, so
+ * the timed applies are the same graph replays as untimed ones; fdh_get_stats
+ * averages the applies recorded since this call).  Resets the averages and
+ * apply_ms_sum. */
 int fdh_set_timing(fdh_op* op, int enable);
 
 int fdh_get_stats(const fdh_op* op, fdh_stats* out);

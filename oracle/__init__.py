@@ -59,6 +59,7 @@ def lib():
         L.orc_leaf_points.argtypes = [C.c_void_p, C.c_int, C.c_int64, _i64, C.c_int64]
         L.orc_leaf_points.restype = C.c_int64
         L.orc_stats.argtypes = [C.c_void_p, _i64]
+        L.orc_last_timing.argtypes = [C.c_void_p, _d]
         for f in ("orc_export_tree", "orc_export_perm", "orc_export_dirsets"):
             getattr(L, f).argtypes = [C.c_void_p, C.c_int, _i64]
             getattr(L, f).restype = C.c_int64
@@ -77,6 +78,9 @@ def lib():
         L.orc_dense_rows.argtypes = [_d, _d, _d, _i64, C.c_int64, _d, _d, _d, C.c_int64, _d, C.c_double, C.c_int, _d]
         L.orc_kernel.argtypes = [_d, C.c_double, _d]
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_structure_digest.argtypes = [_d, _d, _d, C.c_int64, _d, _d, _d, C.c_int64, _d, _d, C.c_double,
+                                           C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                                           _i64]
         L.orc_create_sampled.argtypes = [_d, _d, _d, C.c_int64, _d, _d, _d, C.c_int64, _d, _d, C.c_double, C.c_int,
                                          C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _i64, C.c_int64,
                                          C.POINTER(C.c_void_p)]
@@ -181,6 +185,13 @@ class Oracle:
         rows = np.concatenate([self.leaf_points(0, int(i)) for i in lv]) if len(lv) else np.zeros(0, np.int64)
         return rows, y[rows]
 
+    def last_timing(self):
+        """Seconds of the last apply: upward, coupling generation, M2L products,
+        downward + near field, and the number of coupling matrices generated."""
+        out = np.zeros(5)
+        lib().orc_last_timing(self.h, _p(out))
+        return dict(zip(("upward", "coupling", "m2l", "down_nf", "keys_generated"), out.tolist()))
+
     def leaf_count(self, which=0):
         return lib().orc_leaf_count(self.h, which)
 
@@ -256,6 +267,57 @@ def coupling_matrix(m, kappa, side, d, c):
     s, cc = _f64(side), _f64(c)
     _chk(lib().orc_coupling_matrix(m, float(kappa), _p(s), int(d[0]), int(d[1]), int(d[2]), _p(cc),
                                    out.view(np.float64).ctypes.data_as(_d)))
+    return out
+
+
+DIGEST_NAMES = ["tree_T", "tree_S", "lplus", "lminus", "dirsets_T", "dirsets_S"]
+DIGEST_COUNTS = ["n_c", "n_sc", "n_lminus", "m_d", "nodes_t", "nodes_s", "slots_t", "slots_s", "depth_t", "depth_s",
+                 "l_hf"]
+
+
+def structure_digest(targets, sources, root_lo, root_hi, kappa, n_max=64, eta2=1.0, l_hf=-2, depth_cap=30):
+    """Streaming digest of the full structure (orc_structure_digest): 6 uint64 digests
+    (DIGEST_NAMES) and the counters (DIGEST_COUNTS), without storing L+."""
+    tx, ty, tz = (_f64(a) for a in targets)
+    sx, sy, sz = (_f64(a) for a in sources)
+    lo, hi = _f64(root_lo), _f64(root_hi)
+    out = np.zeros(6, dtype=np.uint64)
+    cnt = np.zeros(11, dtype=np.int64)
+    _chk(lib().orc_structure_digest(_p(tx), _p(ty), _p(tz), len(tx), _p(sx), _p(sy), _p(sz), len(sx), _p(lo), _p(hi),
+                                    float(kappa), int(n_max), 0, float(eta2), int(l_hf), int(depth_cap),
+                                    out.ctypes.data_as(C.POINTER(C.c_uint64)), _pi(cnt)))
+    return [int(v) for v in out], dict(zip(DIGEST_COUNTS, cnt.tolist()))
+
+
+def _mix64(z):
+    z = z + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def rows_digest(rows):
+    """sum over rows (int64 [n, c]) of the splitmix64 row hash, mod 2^64 -- the
+    row digest of orc_structure_digest / fdh_structure_digest, in numpy."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64).view(np.uint64)
+    with np.errstate(over="ignore"):
+        h = np.full(rows.shape[0], 0x12345678, dtype=np.uint64)
+        for c in range(rows.shape[1]):
+            h = _mix64(h ^ rows[:, c])
+        return int(h.sum(dtype=np.uint64))
+
+
+def export_digest(o):
+    """The 6 digests from a full oracle's canonical exports (cross-check of the
+    streaming digest)."""
+    out = []
+    for w in (0, 1):
+        perm = o.perm(w)
+        pr = np.stack([np.arange(len(perm), dtype=np.int64), perm], axis=1)
+        out.append((rows_digest(o.tree(w)) + rows_digest(pr)) % (1 << 64))
+    out.append(rows_digest(o.lplus()))
+    out.append(rows_digest(o.lminus()))
+    out += [rows_digest(o.dirsets(0)), rows_digest(o.dirsets(1))]
     return out
 
 

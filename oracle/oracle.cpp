@@ -27,6 +27,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 
 namespace {
@@ -390,6 +391,10 @@ struct Op {
   // coupling matrices are generated per block in the M2L instead of stored
   std::vector<char> need_t;  // empty = every target box
   bool onthefly = false;
+  // seconds of the last apply: upward pass, coupling generation (sampled mode),
+  // M2L products, L2L + L2T + near field; [4] = coupling matrices generated
+  double tim[5] = {0, 0, 0, 0, 0};
+  double tim_start = 0.0;
 };
 
 bool admissible(const Op& op, int32_t t, int32_t s) {
@@ -587,6 +592,7 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
   const Tree& S = op.S;
   const int n = op.n, m = op.m;
   const double kappa = op.kappa;
+  op.tim_start = omp_get_wtime();
   const int64_t NS = (int64_t)S.perm.size();
   std::vector<cplx> v(NS);  // charges in source slot order
   for (int64_t s = 0; s < NS; ++s) v[s] = cplx(xin[2 * (int64_t)S.perm[s]], xin[2 * (int64_t)S.perm[s] + 1]);
@@ -664,6 +670,74 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
   }
   // (iii) M2L: g~_{t,c} += A_{c,t x s} v~_{s,c}; owner computes over t
   const int64_t nT = (int64_t)T.nodes.size();
+  const double tm0 = omp_get_wtime();
+  op.tim[0] = tm0 - op.tim_start;
+  if (op.onthefly) {
+    // sampled-structure mode: coupling matrices are generated per key, once per
+    // apply for all sampled blocks that use the key (key-major, as a CPU code
+    // without room for the 228 GB coupling set of config 4 would run), the
+    // products of each block kept and summed per target in block order (the
+    // same order as the target-major loop below: deterministic)
+    std::vector<std::pair<int32_t, int64_t>> kb;  // (key, block)
+    for (int64_t t = 0; t < nT; ++t)
+      if (need[t])
+        for (int64_t b = op.lp_ptr[t]; b < op.lp_ptr[t + 1]; ++b) kb.push_back({op.lplus[b].key, b});
+    std::sort(kb.begin(), kb.end());
+    std::vector<int64_t> kstart;
+    for (size_t i = 0; i < kb.size(); ++i)
+      if (i == 0 || kb[i].first != kb[i - 1].first) kstart.push_back((int64_t)i);
+    kstart.push_back((int64_t)kb.size());
+    std::unordered_map<int64_t, int64_t> slot_of_block;  // block -> row of prod
+    slot_of_block.reserve(kb.size() * 2);
+    for (size_t i = 0; i < kb.size(); ++i) slot_of_block[kb[i].second] = (int64_t)i;
+    std::vector<cplx> prod(kb.size() * (size_t)n);
+    double gen_s = 0.0, mv_s = 0.0;
+#pragma omp parallel reduction(+ : gen_s, mv_s)
+    {
+      std::vector<cplx> A((size_t)n * n);
+#pragma omp for schedule(dynamic, 1)
+      for (int64_t k = 0; k < (int64_t)kstart.size() - 1; ++k) {
+        const double g0 = omp_get_wtime();
+        const int32_t key = kb[kstart[k]].first;
+        const auto& kk = op.keys[key];
+        const int kl = std::get<0>(kk);
+        double c[3];
+        dir_vec(kl, op.lhf, op.key_dir[key], c);
+        coupling_matrix(op.m, op.kappa, op.T.side[kl].data(), std::get<1>(kk), std::get<2>(kk), std::get<3>(kk), c,
+                        A.data());
+        const double g1 = omp_get_wtime();
+        for (int64_t i = kstart[k]; i < kstart[k + 1]; ++i) {
+          const Blk& bk = op.lplus[kb[i].second];
+          const int32_t sdi = find_dir(op.dS[bk.s], bk.dir);
+          const cplx* in = &mom[(size_t)(op.slotS[bk.s] + sdi) * n];
+          cplx* out = &prod[(size_t)i * n];
+          for (int j = 0; j < n; ++j) {
+            cplx acc(0, 0);
+            const cplx* Aj = &A[(size_t)j * n];
+            for (int q = 0; q < n; ++q) acc += Aj[q] * in[q];
+            out[j] = acc;
+          }
+        }
+        gen_s += g1 - g0;
+        mv_s += omp_get_wtime() - g1;
+      }
+    }
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t t = 0; t < nT; ++t) {
+      if (!need[t]) continue;
+      for (int64_t b = op.lp_ptr[t]; b < op.lp_ptr[t + 1]; ++b) {
+        const Blk& bk = op.lplus[b];
+        const int32_t tdi = find_dir(op.dT[t], bk.dir);
+        cplx* out = &loc[(size_t)(op.slotT[t] + tdi) * n];
+        const cplx* pr = &prod[(size_t)slot_of_block[b] * n];
+        for (int j = 0; j < n; ++j) out[j] += pr[j];
+      }
+    }
+    const double wall = omp_get_wtime() - tm0;
+    op.tim[1] = (gen_s + mv_s) > 0 ? wall * gen_s / (gen_s + mv_s) : 0.0;  // coupling generation share
+    op.tim[2] = wall - op.tim[1];
+    op.tim[4] = (double)(kstart.size() - 1);
+  } else {
 #pragma omp parallel
   {
   std::vector<cplx> Abuf(op.onthefly ? (size_t)n * n : 0);
@@ -700,6 +774,11 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
     }
   }
   }
+    op.tim[1] = 0.0;
+    op.tim[2] = omp_get_wtime() - tm0;
+    op.tim[4] = 0.0;
+  }
+  const double tm1 = omp_get_wtime();
   // (iv) L2L, levels 0 .. p(T_T)-1: g~_{t',c'} += E_{t',c} g~_{t,c}
   for (int l = 0; l < T.depth; ++l) {
     const auto& lv = T.levels[l];
@@ -795,8 +874,214 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
     }
   }
   op.M_D_zero = zero_skips;
+  op.tim[3] = omp_get_wtime() - tm1;
   (void)zero3;
   if (singular) throw Err(E_DOMAIN, "Helmholtz kernel is singular at x == y (near field)");
+}
+
+// ------------------------------------------------ streaming structure digest
+// Order-independent 64-bit digests of the canonical structure (the same row
+// layouts as the orc_export_* functions; digest = sum over rows of a splitmix64
+// row hash mod 2^64), computed WITHOUT storing the block lists: PAPER Alg. 2
+// (RefineBlock, :136-148) is run depth-first from a frontier of block pairs in
+// parallel, every L+ / L- block is hashed where it is classified, and D(t) is
+// accumulated in per-node direction marks.  Used to pin the structure of the
+// configurations whose L+ does not fit in host memory (config 4: 3.47e9 blocks).
+inline uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+inline uint64_t row_hash(const int64_t* v, int n) {
+  uint64_t h = 0x12345678ull;
+  for (int i = 0; i < n; ++i) h = mix64(h ^ (uint64_t)v[i]);
+  return h;
+}
+
+struct DigestAcc {
+  uint64_t lp = 0, lm = 0;
+  int64_t n_c = 0, n_lm = 0, m_d = 0;
+};
+
+struct DigestCtx {
+  Op* op;
+  std::vector<int64_t> doffT, doffS;                 // first mark of node id
+  std::vector<uint8_t> markT, markS;                 // D marks (bit 0), D^ (bit 1)
+  std::vector<std::vector<uint64_t>> keybits;        // per level, dense key bitmap (levels <= 8)
+  std::vector<int64_t> kext;                         // per level: offsets in (-kext, kext)
+};
+
+inline int key_dir_of(const Op& op, int l, int64_t dx, int64_t dy, int64_t dz) {
+  const double v[3] = {dx * op.rho[0], dy * op.rho[1], dz * op.rho[2]};
+  return dir_map_vec(l, op.lhf, v);
+}
+
+void digest_block(DigestCtx& X, DigestAcc& A, int32_t t, int32_t s, std::vector<std::array<int64_t, 4>>& deep) {
+  Op& op = *X.op;
+  const Node& nt = op.T.nodes[t];
+  const Node& ns = op.S.nodes[s];
+  const bool adm = admissible(op, t, s);
+  const int l = nt.c.level;
+  if (nt.leaf || ns.leaf || adm) {
+    if (adm) {
+      const int64_t dx = nt.c.i - ns.c.i, dy = nt.c.j - ns.c.j, dz = nt.c.k - ns.c.k;
+      const int dir = key_dir_of(op, l, dx, dy, dz);
+      const int64_t r[8] = {l, nt.c.i, nt.c.j, nt.c.k, ns.c.i, ns.c.j, ns.c.k, dir};
+      A.lp += row_hash(r, 8);
+      ++A.n_c;
+      __atomic_fetch_or(&X.markT[X.doffT[t] + dir], (uint8_t)1, __ATOMIC_RELAXED);
+      __atomic_fetch_or(&X.markS[X.doffS[s] + dir], (uint8_t)1, __ATOMIC_RELAXED);
+      if (l < (int)X.keybits.size()) {
+        const int64_t e = X.kext[l], w = 2 * e + 1;
+        const uint64_t bit = (uint64_t)(((dx + e) * w + (dy + e)) * w + (dz + e));
+        __atomic_fetch_or(&X.keybits[l][bit >> 6], 1ull << (bit & 63), __ATOMIC_RELAXED);
+      } else {
+        deep.push_back({l, dx, dy, dz});
+      }
+    } else {
+      const int64_t r[8] = {l, nt.c.i, nt.c.j, nt.c.k, l, ns.c.i, ns.c.j, ns.c.k};
+      A.lm += row_hash(r, 8);
+      ++A.n_lm;
+      A.m_d += (int64_t)nt.count() * ns.count();
+    }
+    return;
+  }
+  for (int a = 0; a < 8; ++a) {
+    if (nt.child[a] < 0) continue;
+    for (int b = 0; b < 8; ++b)
+      if (ns.child[b] >= 0) digest_block(X, A, nt.child[a], ns.child[b], deep);
+  }
+}
+
+void structure_digest_stream(Op& op, uint64_t out[6], int64_t* cnt) {
+  Tree& T = op.T;
+  Tree& S = op.S;
+  if (op.lhf == -2) {  // same rule as build_structure
+    op.lhf = -1;
+    for (int l = 0; l <= std::min(T.depth, S.depth); ++l)
+      if (op.kappa * std::max(T.diam[l], S.diam[l]) >= 3.0) op.lhf = l;
+  }
+  const double mn = std::min({T.side[0][0], T.side[0][1], T.side[0][2]});
+  for (int a = 0; a < 3; ++a) op.rho[a] = T.side[0][a] / mn;
+  DigestCtx X;
+  X.op = &op;
+  auto offs = [&](const Tree& tr, std::vector<int64_t>& off, std::vector<uint8_t>& mark) {
+    off.resize(tr.nodes.size() + 1);
+    int64_t acc = 0;
+    for (size_t id = 0; id < tr.nodes.size(); ++id) {
+      off[id] = acc;
+      acc += num_dirs(tr.nodes[id].c.level, op.lhf);
+    }
+    off[tr.nodes.size()] = acc;
+    mark.assign(acc, 0);
+  };
+  offs(T, X.doffT, X.markT);
+  offs(S, X.doffS, X.markS);
+  const int maxl = std::min(T.depth, S.depth);
+  for (int l = 0; l <= std::min(maxl, 8); ++l) {
+    const int64_t e = (int64_t)1 << l, w = 2 * e + 1;
+    X.kext.push_back(e);
+    X.keybits.emplace_back((size_t)((w * w * w + 63) / 64), 0ull);
+  }
+  // frontier: breadth-first until there are enough independent pairs
+  std::vector<std::pair<int32_t, int32_t>> front{{0, 0}};
+  DigestAcc A0;
+  std::vector<std::array<int64_t, 4>> deep0;
+  for (int it = 0; it < 4 && front.size() < 4096; ++it) {
+    std::vector<std::pair<int32_t, int32_t>> nxt;
+    for (auto [t, s] : front) {
+      const Node& nt = T.nodes[t];
+      const Node& ns = S.nodes[s];
+      if (nt.leaf || ns.leaf || admissible(op, t, s)) {
+        digest_block(X, A0, t, s, deep0);  // classified here
+        continue;
+      }
+      for (int a = 0; a < 8; ++a) {
+        if (nt.child[a] < 0) continue;
+        for (int b = 0; b < 8; ++b)
+          if (ns.child[b] >= 0) nxt.push_back({nt.child[a], ns.child[b]});
+      }
+    }
+    front.swap(nxt);
+  }
+  uint64_t lp = A0.lp, lm = A0.lm;
+  int64_t n_c = A0.n_c, n_lm = A0.n_lm, m_d = A0.m_d;
+  std::vector<std::array<int64_t, 4>> deep = deep0;
+#pragma omp parallel
+  {
+    DigestAcc A;
+    std::vector<std::array<int64_t, 4>> dp;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t i = 0; i < (int64_t)front.size(); ++i) digest_block(X, A, front[i].first, front[i].second, dp);
+#pragma omp critical
+    {
+      lp += A.lp;
+      lm += A.lm;
+      n_c += A.n_c;
+      n_lm += A.n_lm;
+      m_d += A.m_d;
+      deep.insert(deep.end(), dp.begin(), dp.end());
+    }
+  }
+  // N_SC: distinct (level, offset) keys
+  int64_t n_sc = 0;
+  for (auto& kb : X.keybits)
+    for (uint64_t w : kb) n_sc += __builtin_popcountll(w);
+  std::sort(deep.begin(), deep.end());
+  n_sc += (int64_t)(std::unique(deep.begin(), deep.end()) - deep.begin());
+  // D^ (Def. 4): parent's D u D^ mapped to the child level, pre-order by level
+  auto hat = [&](Tree& tr, const std::vector<int64_t>& off, std::vector<uint8_t>& mark) {
+    for (int l = 1; l <= tr.depth; ++l)
+      for (int32_t id : tr.levels[l]) {
+        const int32_t par = tr.nodes[id].parent;
+        const int npd = num_dirs(l - 1, op.lhf);
+        for (int c = 0; c < npd; ++c)
+          if (mark[off[par] + c]) mark[off[id] + parent_dir(l - 1, op.lhf, c)] |= 2;
+      }
+  };
+  hat(T, X.doffT, X.markT);
+  hat(S, X.doffS, X.markS);
+  int64_t slots[2] = {0, 0};
+  for (int w = 0; w < 2; ++w) {
+    const Tree& tr = w == 0 ? T : S;
+    const auto& off = w == 0 ? X.doffT : X.doffS;
+    const auto& mark = w == 0 ? X.markT : X.markS;
+    uint64_t acc = 0, dacc = 0;
+    for (size_t id = 0; id < tr.nodes.size(); ++id) {
+      const Node& nd = tr.nodes[id];
+      const int64_t r[7] = {nd.c.level, nd.c.i, nd.c.j, nd.c.k, nd.begin, nd.end, nd.leaf ? 1 : 0};
+      acc += row_hash(r, 7);
+      for (int64_t c = 0; c < off[id + 1] - off[id]; ++c) {
+        const uint8_t k = mark[off[id] + c];
+        if (!k) continue;
+        const int64_t rr[6] = {nd.c.level, nd.c.i, nd.c.j, nd.c.k, c, k};
+        dacc += row_hash(rr, 6);
+        ++slots[w];
+      }
+    }
+    for (size_t sl = 0; sl < tr.perm.size(); ++sl) {
+      const int64_t r[2] = {(int64_t)sl, (int64_t)tr.perm[sl]};
+      acc += row_hash(r, 2);
+    }
+    out[w] = acc;
+    out[4 + w] = dacc;
+  }
+  out[2] = lp;
+  out[3] = lm;
+  if (cnt) {
+    cnt[0] = n_c;
+    cnt[1] = n_sc;
+    cnt[2] = n_lm;
+    cnt[3] = m_d;
+    cnt[4] = (int64_t)T.nodes.size();
+    cnt[5] = (int64_t)S.nodes.size();
+    cnt[6] = slots[0];
+    cnt[7] = slots[1];
+    cnt[8] = T.depth;
+    cnt[9] = S.depth;
+    cnt[10] = op.lhf;
+  }
 }
 
 template <class F>
@@ -892,6 +1177,24 @@ int orc_create_sampled(const double* tx, const double* ty, const double* tz, int
                      false, out, leaf_idx, nleaf);
 }
 void orc_destroy(orc_op* op) { delete op; }
+int orc_structure_digest(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
+                         const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
+                         double kappa, int n_max, int m_unused, double eta2, int l_hf, int depth_cap,
+                         uint64_t* out6, int64_t* counts) {
+  return guard([&] {
+    if (!(kappa > 0.0) || !std::isfinite(kappa)) throw Err(E_ARG, "wave number must be positive and finite");
+    if (!(eta2 > 0.0)) throw Err(E_ARG, "eta2 must be positive");
+    if (l_hf < -2) throw Err(E_ARG, "l_hf must be >= -1 (or -2 for the default rule)");
+    (void)m_unused;
+    Op op;
+    op.kappa = kappa;
+    op.eta2 = eta2;
+    op.lhf = l_hf;
+    op.T.build(tx, ty, tz, nt, lo, hi, n_max, depth_cap);
+    op.S.build(sx, sy, sz, ns, lo, hi, n_max, depth_cap);
+    structure_digest_stream(op, out6, counts);
+  });
+}
 
 int orc_apply(orc_op* o, const double* x, double* y) {
   return guard([&] {
@@ -912,6 +1215,10 @@ int orc_apply_sampled(orc_op* o, const double* x, const int64_t* leaf_idx, int64
     }
     apply(o->op, x, y, &mask);
   });
+}
+int orc_last_timing(const orc_op* o, double* out5) {
+  for (int i = 0; i < 5; ++i) out5[i] = o->op.tim[i];
+  return 0;
 }
 int64_t orc_leaf_count(const orc_op* o, int which) {
   return (int64_t)(which == 0 ? o->op.T : o->op.S).leaves.size();

@@ -68,6 +68,18 @@ int orc_create_sampled(const double* tx, const double* ty, const double* tz, int
                        double eta2, int l_hf, int depth_cap, int zero_diagonal,
                        const int64_t* leaf_idx, int64_t nleaf, orc_op** out);
 void orc_destroy(orc_op* op);
+/* Streaming structure digest (no block lists stored; config 4 has 3.47e9 L+
+ * blocks): both trees, then Alg. 2 depth-first in parallel, hashing every L+ /
+ * L- block where it is classified.  out6 = order-independent sums of a
+ * splitmix64 row hash over the canonical export rows: [T tree + perm, S tree +
+ * perm, L+, L-, D/D^ of T, D/D^ of S] (the layout fdh_structure_digest uses).
+ * counts[11] = N_C, N_SC, #L-, M_D, nodes_T, nodes_S, slots_T, slots_S,
+ * depth_T, depth_S, l_hf.  m is unused (the structure does not depend on it). */
+int orc_structure_digest(const double* tx, const double* ty, const double* tz, int64_t nt,
+                         const double* sx, const double* sy, const double* sz, int64_t ns,
+                         const double root_lo[3], const double root_hi[3], double kappa, int n_max,
+                         int m, double eta2, int l_hf, int depth_cap, uint64_t* out6,
+                         int64_t* counts);
 const char* orc_last_error(void);
 int orc_set_threads(int n);
 
@@ -84,6 +96,10 @@ int64_t orc_leaf_count(const orc_op* op, int which);
 int64_t orc_leaf_points(const orc_op* op, int which, int64_t leaf, int64_t* idx, int64_t cap);
 
 int orc_stats(const orc_op* op, int64_t* out /* ORC_NSTATS */);
+/* Wall seconds of the last apply: [0] upward pass (S2M + M2M), [1] coupling
+ * matrix generation (sampled-structure mode: once per key used), [2] M2L
+ * products, [3] L2L + L2T + near field; [4] = coupling matrices generated. */
+int orc_last_timing(const orc_op* op, double* out5);
 
 /* Canonical exports.  Each returns the row count; pass
  * out == NULL to query.  Rows are int64 and sorted lexicographically. */

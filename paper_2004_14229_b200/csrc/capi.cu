@@ -99,6 +99,16 @@ struct fdh_op {
   bool overlap_nf = false;
   int nsm = 148, nf_ctas = 1;  // persistent near-field grid when overlapped
   int ring_n = 0;                                 // applies recorded since the last reset
+  int ring_done = 0;                              // ring entries already accumulated
+  // timing inside the CUDA graph: the phase events are captured as external
+  // event-record nodes (gev), read back after each replay
+  cudaEvent_t gev[FDH_NPHASES + 6] = {};
+  bool capturing_timed = false, gtimed = false, gpending = false;
+  double tacc[FDH_NPHASES + 1] = {};              // accumulated phase / M2L-kernel ms
+  int64_t tacc_n = 0;
+  bool fresh = false;                              // ev_all holds an apply not yet collected
+  double apply_ms_sum = 0.0;
+  int64_t applies_collected = 0;
   cudaEvent_t ev[FDH_NPHASES + 1] = {};
   cudaEvent_t ev_all[2] = {};
   fdh_stats stats{};
@@ -126,6 +136,8 @@ struct fdh_op {
     for (auto& r : ring)
       for (auto& e : r)
         if (e) cudaEventDestroy(e);
+    for (auto& e : gev)
+      if (e) cudaEventDestroy(e);
     if (st2) cudaStreamSynchronize(st2);
     if (ev_q) cudaEventDestroy(ev_q);
     if (ev_nf) cudaEventDestroy(ev_nf);
@@ -174,6 +186,7 @@ void setup_device(fdh_op* o) {
   for (auto& e : o->ev_all) CK(cudaEventCreate(&e));
   for (auto& r : o->ring)
     for (auto& e : r) CK(cudaEventCreate(&e));
+  for (auto& e : o->gev) CK(cudaEventCreate(&e));
   // constants
   Consts C{};
   C.kappa = P.prm.kappa;
@@ -322,6 +335,7 @@ void setup_device(fdh_op* o) {
   o->xin = o->alloc<double2>((size_t)(R * o->ns));
   o->yout = o->alloc<double2>((size_t)(R * o->nt));
   o->flag = o->alloc<int>(1);
+  CK(cudaMemset(o->flag, 0, sizeof(int)));  // sticky between fdh_sync calls (device path)
   // coupling matrices: resident when they fit (70 % of the free
   // memory), else generated per apply in segments of key chunks (config 4: 240 GB)
   size_t fre = 0, tot = 0;
@@ -361,7 +375,7 @@ void setup_device(fdh_op* o) {
     if (!o->w_resident && (double)mq > 0.3 * (double)fre) throw PlanError{-1, "int8 moment digits do not fit"};
     o->Mq = o->alloc<int8_t>((size_t)std::max<int64_t>(mq, 16));
     o->lvmax_w = o->alloc<unsigned long long>(kMaxLevels);
-    o->lvmax_v = o->alloc<unsigned long long>(kMaxLevels);
+    o->lvmax_v = o->alloc<unsigned long long>(kMaxLevels * R);  // per (rhs, level)
     CK(cudaMemsetAsync(o->Mq, 0, (size_t)std::max<int64_t>(mq, 16), o->st));
     CK(cudaMemsetAsync(o->lvmax_w, 0, sizeof(unsigned long long) * kMaxLevels, o->st));
     o->tile_level_d = o->up(P.tile_level);
@@ -406,7 +420,11 @@ void setup_device(fdh_op* o) {
 }
 
 void rec(fdh_op* o, int ph, cudaStream_t st) {
-  if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][ph], st));
+  if (!o->timing) return;
+  if (o->capturing_timed)  // an event-record node of the graph being captured
+    CK(cudaEventRecordWithFlags(o->gev[ph], st, cudaEventRecordExternal));
+  else
+    CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][ph], st));
 }
 
 // Alg. 4 on the device: x_dev (original order) -> y_dev (original order); with
@@ -421,7 +439,6 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   int64_t L = 0;
   if (outer_events) CK(cudaEventRecord(o->ev_all[0], st));  // (graph replays record them around the launch)
   rec(o, FDH_PHASE_H2D, st);
-  CK(cudaMemsetAsync(o->flag, 0, sizeof(int), st));
   for (int r = 0; r < R; ++r)
     launch_gather_charges(st, o->ns, o->perm_s, x + r * o->ns, o->q + r * o->ns, o->q4 + r * o->ns);
   L += R;
@@ -438,19 +455,17 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     L += R;
   }
   rec(o, FDH_PHASE_M2L, st);
-  // near field (vi).  Sequential (default for the FP64 DMMA M2L, which shares the
-  // FP64 pipe with it): on the main stream after the M2L.  overlap_nf (default for
-  // the int8 M2L: tensor pipe vs FP64 pipe): launched on the second stream BEFORE
-  // the M2L as a persistent grid of nf_ctas CTAs per SM, so one near-field CTA
-  // (20 KB shared memory, 128 threads) is resident beside each M2L CTA and the
-  // two run concurrently on different pipes.
+  // near field (vi).  Sequential by default: on the main stream after the M2L.
+  // FDH_OVERLAP_NEARFIELD=1 opts in to launching it on the second stream BEFORE
+  // the M2L as a persistent grid of nf_ctas CTAs per SM (one near-field CTA beside
+  // each M2L CTA, different pipes); measured no faster.
   auto near_field = [&](cudaStream_t snf, int grid) {
-    if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 3], snf));
+    rec(o, FDH_NPHASES + 3, snf);
     launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
                o->tz, o->sx, o->sy, o->sz, o->q4, o->diag_slot, nullptr, P.prm.zero_diagonal, o->ynear, o->flag,
                o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt, grid);
     L += (o->n_leaf > 0) * p2p_launches(R);
-    if (o->timing) CK(cudaEventRecord(o->ring[o->ring_n % fdh_op::kRing][FDH_NPHASES + 4], snf));
+    rec(o, FDH_NPHASES + 4, snf);
   };
   if (o->overlap_nf) {
     CK(cudaEventRecord(o->ev_q, st));  // charges ready: the near field may start
@@ -487,6 +502,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.n_pad = np;
     a.fkeys = P.prm.m2l_fkeys;
     a.n_tile = o->n_tile;
+    a.nrhs = R;
     const int ng = m2l_i8_groups(n);
     rec(o, FDH_NPHASES + 1, st);
     if (o->w_resident) {
@@ -581,19 +597,25 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   CK(cudaGetLastError());
   o->launches = L;
   o->applied = true;
-  if (o->timing) ++o->ring_n;
+  if (outer_events) o->fresh = true;
+  if (o->timing && !o->capturing_timed) ++o->ring_n;
 }
 
 // apply_device through a CUDA graph: ~10-20 kernel launches + memsets per apply
 // become one graph launch (capture in relaxed mode: cudaFuncSetAttribute is
 // called inside).  Any capture / instantiate failure disables graphs for the
 // operator and the apply runs directly.
+void collect_times(fdh_op* o);
 void apply_graph(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
-  if (o->timing || !o->graphs || o->graph_failed) {
+  if (!o->graphs || o->graph_failed) {
     apply_device(o, x, y, st);
     return;
   }
-  if (!(o->gexec && o->gx == x && o->gy == y && o->gst == st)) {
+  if (o->gpending) {  // the previous replay's phase events must be read before they are re-recorded
+    CK(cudaEventSynchronize(o->ev_all[1]));
+    collect_times(o);
+  }
+  if (!(o->gexec && o->gx == x && o->gy == y && o->gst == st && o->gtimed == o->timing)) {
     if (o->gexec) {
       CK(cudaGraphExecDestroy(o->gexec));
       o->gexec = nullptr;
@@ -601,11 +623,13 @@ void apply_graph(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     cudaGraph_t g = nullptr;
     bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
     if (ok) {
+      o->capturing_timed = o->timing;
       try {
         apply_device(o, x, y, st, false);
       } catch (...) {
         ok = false;
       }
+      o->capturing_timed = false;
       ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok && g != nullptr;
     }
     if (ok) ok = cudaGraphInstantiate(&o->gexec, g, 0) == cudaSuccess;
@@ -620,46 +644,66 @@ void apply_graph(fdh_op* o, const double2* x, double2* y, cudaStream_t st) {
     o->gx = x;
     o->gy = y;
     o->gst = st;
+    o->gtimed = o->timing;
   }
   CK(cudaEventRecord(o->ev_all[0], st));
   CK(cudaGraphLaunch(o->gexec, st));
   CK(cudaEventRecord(o->ev_all[1], st));
   o->applied = true;
+  o->fresh = true;
+  if (o->gtimed) o->gpending = true;
   ++o->graph_replays;
+}
+
+// per-phase times of one apply from its event set (ring entry or graph events)
+void phase_times(fdh_op* o, cudaEvent_t* E, double* acc) {
+  float ms = 0;
+  for (int ph = 0; ph < FDH_NPHASES; ++ph) {
+    CK(cudaEventElapsedTime(&ms, E[ph], E[ph + 1]));
+    acc[ph] += ms;
+  }
+  if (o->n_item > 0) {
+    CK(cudaEventElapsedTime(&ms, E[FDH_NPHASES + 1], E[FDH_NPHASES + 2]));
+    acc[FDH_NPHASES] += ms;
+  }
+  // L2T excludes the wait for the concurrent near field
+  CK(cudaEventElapsedTime(&ms, E[FDH_PHASE_L2T], E[FDH_PHASE_L2T + 1]));
+  acc[FDH_PHASE_L2T] -= ms;
+  CK(cudaEventElapsedTime(&ms, E[FDH_NPHASES + 5], E[FDH_PHASE_L2T + 1]));
+  acc[FDH_PHASE_L2T] += ms;
+  CK(cudaEventElapsedTime(&ms, E[FDH_NPHASES + 3], E[FDH_NPHASES + 4]));
+  acc[FDH_PHASE_P2P] += ms;  // replaces the (empty) P2P slot between L2T and D2H
+  if (!o->overlap_nf) acc[FDH_PHASE_M2L] -= ms;  // sequential: it ran inside the M2L interval
+  CK(cudaEventElapsedTime(&ms, E[FDH_PHASE_P2P], E[FDH_PHASE_P2P + 1]));
+  acc[FDH_PHASE_P2P] -= ms;
 }
 
 void collect_times(fdh_op* o) {
   if (!o->applied) return;
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, o->ev_all[0], o->ev_all[1]));
-  o->stats.apply_ms = ms;
-  // per-phase averages over the applies recorded since the last fdh_set_timing
-  const int nr = std::min(o->ring_n, fdh_op::kRing);
-  if (nr > 0) {
-    double acc[FDH_NPHASES + 1] = {0};
-    for (int r = 0; r < nr; ++r) {
-      for (int ph = 0; ph < FDH_NPHASES; ++ph) {
-        CK(cudaEventElapsedTime(&ms, o->ring[r][ph], o->ring[r][ph + 1]));
-        acc[ph] += ms;
-      }
-      if (o->n_item > 0) {
-        CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 1], o->ring[r][FDH_NPHASES + 2]));
-        acc[FDH_NPHASES] += ms;
-      }
-      // L2T excludes the wait for the concurrent near field
-      CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_PHASE_L2T], o->ring[r][FDH_PHASE_L2T + 1]));
-      acc[FDH_PHASE_L2T] -= ms;
-      CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 5], o->ring[r][FDH_PHASE_L2T + 1]));
-      acc[FDH_PHASE_L2T] += ms;
-      CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_NPHASES + 3], o->ring[r][FDH_NPHASES + 4]));
-      acc[FDH_PHASE_P2P] += ms;  // replaces the (empty) P2P slot between L2T and D2H
-      if (!o->overlap_nf) acc[FDH_PHASE_M2L] -= ms;  // sequential: it ran inside the M2L interval
-      CK(cudaEventElapsedTime(&ms, o->ring[r][FDH_PHASE_P2P], o->ring[r][FDH_PHASE_P2P + 1]));
-      acc[FDH_PHASE_P2P] -= ms;
-    }
-    for (int ph = 0; ph < FDH_NPHASES; ++ph) o->stats.phase_ms[ph] = acc[ph] / nr;
-    o->stats.m2l_gemm_ms = acc[FDH_NPHASES] / nr;
-    o->stats.timed_applies = nr;
+  if (o->fresh) {
+    CK(cudaEventElapsedTime(&ms, o->ev_all[0], o->ev_all[1]));
+    o->stats.apply_ms = ms;
+    o->apply_ms_sum += ms;
+    ++o->applies_collected;
+    o->fresh = false;
+  }
+  // phase times accumulated since the last fdh_set_timing: graph replays (one
+  // event set, read after each replay) and direct launches (ring of 64)
+  if (o->gpending) {
+    phase_times(o, o->gev, o->tacc);
+    ++o->tacc_n;
+    o->gpending = false;
+  }
+  if (o->ring_n - o->ring_done > fdh_op::kRing) o->ring_done = o->ring_n - fdh_op::kRing;
+  for (; o->ring_done < o->ring_n; ++o->ring_done) {
+    phase_times(o, o->ring[o->ring_done % fdh_op::kRing], o->tacc);
+    ++o->tacc_n;
+  }
+  if (o->tacc_n > 0) {
+    for (int ph = 0; ph < FDH_NPHASES; ++ph) o->stats.phase_ms[ph] = o->tacc[ph] / o->tacc_n;
+    o->stats.m2l_gemm_ms = o->tacc[FDH_NPHASES] / o->tacc_n;
+    o->stats.timed_applies = o->tacc_n;
   }
 }
 
@@ -807,6 +851,7 @@ int fdh_apply_multi(fdh_op* o, const double* x, int64_t k, double* y) {
         CK(cudaMemsetAsync(o->xin + nb * o->ns, 0, sizeof(double2) * (size_t)((R - nb) * o->ns), o->st));
       CK(cudaMemcpyAsync(o->xin, x + 2 * b * o->ns, sizeof(double2) * (size_t)(nb * o->ns), cudaMemcpyHostToDevice,
                          o->st));
+      CK(cudaMemsetAsync(o->flag, 0, sizeof(int), o->st));
       apply_graph(o, o->xin, o->yout, o->st);
       CK(cudaMemcpyAsync(y + 2 * b * o->nt, o->yout, sizeof(double2) * (size_t)(nb * o->nt),
                          cudaMemcpyDeviceToHost, o->st));
@@ -831,13 +876,37 @@ int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream
   });
 }
 
+int fdh_sync(fdh_op* o) {
+  if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  if (!o->st) return FDH_OK;
+  return guard([&] {
+    CK(cudaSetDevice(o->device));
+    CK(cudaStreamSynchronize(o->st));
+    if (o->gst && o->gst != o->st) CK(cudaStreamSynchronize(o->gst));
+    int flag = 0;
+    CK(cudaMemcpy(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(o->flag, 0, sizeof(int)));
+    if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
+    if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+  });
+}
+
 void* fdh_stream(fdh_op* o) { return o ? static_cast<void*>(o->st) : nullptr; }
 
 int fdh_set_timing(fdh_op* o, int enable) {
   if (!o) return fail(FDH_ERR_ARG, "NULL op");
-  o->timing = enable != 0;
-  o->ring_n = 0;
-  return FDH_OK;
+  return guard([&] {
+    if (o->st) {
+      CK(cudaStreamSynchronize(o->st));
+      collect_times(o);  // flush what the previous mode recorded
+    }
+    o->timing = enable != 0;
+    o->ring_n = o->ring_done = 0;
+    o->tacc_n = 0;
+    for (double& v : o->tacc) v = 0.0;
+    o->apply_ms_sum = 0.0;
+    o->applies_collected = 0;
+  });
 }
 
 int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
@@ -882,6 +951,8 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->w_segments = (int64_t)o->segs.size();
   s->nrhs = o->R;
   s->graph_replays = o->graph_replays;
+  s->apply_ms_sum = o->apply_ms_sum;
+  s->applies_collected = o->applies_collected;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

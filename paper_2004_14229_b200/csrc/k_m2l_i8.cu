@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
   }
 }
 
-// moments: per-level max (pass 0), then digits of every source slot (pass 1):
+// moments: per-(rhs, level) max (pass 0), then digits of every source slot (pass 1):
 // Mq: per (slot, K chunk of 32) one contiguous block of KS x 2 (kb) x 2 (h) x 16 B
 // = the pieces a gather warp copies with consecutive lanes; digit i of row h,
 // h = 0: [Re v | -Im v], h = 1: [Im v | Re v] (K index kk < n_kq: first half)
@@ -256,7 +256,11 @@ __global__ void __launch_bounds__(128) k_mom_max(const double* __restrict__ mom,
   __syncthreads();
   if (threadIdx.x == 0) {
     mx = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
-    if (mx > 0.0) atomicMax(lvmax + slot_level[s % nslot1], (unsigned long long)__double_as_longlong(mx));
+    // one scale per (rhs, level): a vector of a batch is never rounded against a
+    // larger vector's scale (batching must not change results)
+    if (mx > 0.0)
+      atomicMax(lvmax + (s / nslot1) * kMaxLevels + slot_level[s % nslot1],
+                (unsigned long long)__double_as_longlong(mx));
   }
 }
 template <int KS>
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
                                                    int nkq, int8_t* __restrict__ Mq, int64_t nslot1) {
   const int64_t s = blockIdx.x;
   const double* g = mom + s * 2 * n_pad;
-  const int ex = level_exp(lvmax, slot_level[s % nslot1]);
+  const int ex = level_exp(lvmax, (int)(s / nslot1) * kMaxLevels + slot_level[s % nslot1]);
   const int kp = 2 * nkq;
   const int nch = kp / kKC;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -311,7 +315,7 @@ __global__ void __maxnreg__(128)
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
              int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys, int mb_tot, int grp, int tick_off,
-             int64_t key_base) {
+             int64_t key_base, int nrhs) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int NT = S::THREADS;
@@ -487,7 +491,10 @@ __global__ void __maxnreg__(128)
   // ---- epilogue: levels -> FP64, chained accumulation into the tile
   const int seq = item_seq[item], nit = tile_nitem[tile];
   const int lvl = tile_level[tile];
-  const int exs = level_exp(lvmax_w, lvl) + level_exp(lvmax_v, lvl) + 2;
+  const int exw = level_exp(lvmax_w, lvl) + 2;
+  __shared__ double csc[TT];  // S_W S_V of each tile column (its rhs' moment scale)
+  if (tid < TT) csc[tid] = ldexp(1.0, exw + level_exp(lvmax_v, (tid % nrhs) * kMaxLevels + lvl));
+  __syncthreads();
   if (seq > 0) {
     if (tid == 0) {
       long long spins = 0;
@@ -502,9 +509,10 @@ __global__ void __maxnreg__(128)
     __syncthreads();
   }
   const bool last = seq == nit - 1;
-  double fL[S::LV];  // level weights 2^(-7(L+2)) S_W S_V
+  double fL[S::LV];  // level weights 2^(-7(L+2)); the power-of-two scale S_W S_V of the
+                    // column's rhs is applied after the (exact) level sum
 #pragma unroll
-  for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, exs - 7 * (L + 2));
+  for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
   double* A = tile_acc + (int64_t)tile * n_pad * NC;
   const int qw = warp & 3;  // TMEM lane quarter of this warp
 #pragma unroll 1
@@ -524,7 +532,7 @@ __global__ void __maxnreg__(128)
         double a = 0.0;
 #pragma unroll
         for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
-        v[e] = a;
+        v[e] = a * csc[(8 * g + e) >> 1];  // exact: a power of two
       }
       double* pa = A + (int64_t)row * NC + 8 * g;
       if (seq > 0) {
@@ -569,7 +577,7 @@ void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int grp) {
   kern<<<a.n_item, S::THREADS, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
                                          a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
                                          a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.err, a.item0, a.nkq,
-                                         a.n_pad, a.fkeys, mb_tot, grp, grp * a.n_tile, a.key_base);
+                                         a.n_pad, a.fkeys, mb_tot, grp, grp * a.n_tile, a.key_base, a.nrhs);
 }
 
 }  // namespace
@@ -598,7 +606,7 @@ void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, 
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
                       int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs) {
   if (nslots <= 0) return;
-  cudaMemsetAsync(lvmax_v, 0, sizeof(unsigned long long) * kMaxLevels, st);
+  cudaMemsetAsync(lvmax_v, 0, sizeof(unsigned long long) * kMaxLevels * nrhs, st);
   const unsigned nb = (unsigned)(nslots * nrhs);
   k_mom_max<<<nb, 128, 0, st>>>(mom, slot_level, n, n_pad, lvmax_v, nslots);
   k_mom_quant<kI8Digits><<<nb, 128, 0, st>>>(mom, slot_level, lvmax_v, n, n_pad, nkq, Mq, nslots);

@@ -662,6 +662,57 @@ __global__ void k_mark_dhat(int64_t nn, const int32_t* __restrict__ parent, cons
     }
 }
 
+// order-independent digest of the L+ rows (level, t coord, s coord, dir): sum of a
+// splitmix64 row hash, the layout of plan.cpp structure_digest / oracle.cpp
+__device__ __forceinline__ unsigned long long dmix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_lplus_digest(int64_t nb, FDH_PAIR_ARGS, const int32_t* __restrict__ key,
+                               const int32_t* __restrict__ kdir, int level, unsigned long long* __restrict__ acc) {
+  __shared__ unsigned long long sh[256];
+  unsigned long long a = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = lpt[b], s = lps[b];
+    const long long r[8] = {level, tci[t], tcj[t], tck[t], sci[s], scj[s], sck[s], kdir[key[b]]};
+    unsigned long long h = 0x12345678ull;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h = dmix64(h ^ (unsigned long long)r[i]);
+    a += h;
+  }
+  sh[threadIdx.x] = a;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicAdd(acc, sh[0]);  // integer sum mod 2^64: exact in any order
+}
+// #L+ per target node (shard cost model); integer atomics, order-independent
+__global__ void k_count_targets(int64_t nb, const int32_t* __restrict__ lpt, int32_t* __restrict__ cnt) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) atomicAdd(cnt + lpt[b], 1);
+}
+// keep the L+ blocks whose target is needed by this shard: flag, scan, stable emit
+__global__ void k_needed_flags(int64_t nb, const int32_t* __restrict__ lpt, const uint8_t* __restrict__ need,
+                               int64_t* __restrict__ f) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) f[b] = need[lpt[b]] ? 1 : 0;
+}
+__global__ void k_needed_emit(int64_t nb, const int32_t* __restrict__ lpt, const int32_t* __restrict__ lps,
+                              const int32_t* __restrict__ key, const uint8_t* __restrict__ need,
+                              const int64_t* __restrict__ pos, int32_t* __restrict__ ot, int32_t* __restrict__ os,
+                              int32_t* __restrict__ ok) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb || !need[lpt[b]]) return;
+  const int64_t o = pos[b];
+  ot[o] = lpt[b];
+  os[o] = lps[b];
+  ok[o] = key[b];
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ public
@@ -847,12 +898,69 @@ void gpu_build_structure(Plan& P, const double* tx, const double* ty, const doub
     }
     X.nslots = s;
   }
+  // digest of the full L+ (the shard keeps only part of it on the host)
+  {
+    unsigned long long* acc = D.alloc<unsigned long long>(1);
+    SCK(cudaMemset(acc, 0, sizeof(unsigned long long)));
+    for (int l = 0; l <= maxl; ++l)
+      if (nlp[l] > 0)
+        k_lplus_digest<<<std::min<unsigned>(148 * 16, nblocks(nlp[l])), 256>>>(
+            nlp[l], lpt[l], lps[l], dT[l].ci, dT[l].cj, dT[l].ck, dS[l].ci, dS[l].cj, dS[l].ck, lpk[l], kdir_all, l,
+            acc);
+    SCK(cudaGetLastError());
+    P.lplus_digest = down(acc, 1)[0];
+    P.lplus_digest_dev = true;
+    D.release(acc);
+  }
+  P.n_c = 0;
+  for (int l = 0; l <= maxl; ++l) P.n_c += nlp[l];
+  // shards: the cost model from per-target L+ counts, ownership
+  // and its ancestor closure on the host, then only the L+ blocks with a needed
+  // target go to the host (config 4, rank r of 8: ~1/8 of the 3.47e9 blocks)
+  const bool shard = P.prm.world > 1;
+  if (shard) {
+    P.lp_count.assign(maxl + 1, {});
+    for (int l = 0; l <= maxl; ++l) {
+      int32_t* cnt = D.alloc<int32_t>(dT[l].n);
+      SCK(cudaMemset(cnt, 0, sizeof(int32_t) * dT[l].n));
+      if (nlp[l] > 0) k_count_targets<<<nblocks(nlp[l]), 256>>>(nlp[l], lpt[l], cnt);
+      SCK(cudaGetLastError());
+      P.lp_count[l] = down(cnt, dT[l].n);
+      D.release(cnt);
+    }
+    compute_ownership(P);
+  }
   // L+ lists back to the host (the M2L tiles are assembled there)
+  int64_t kChunk = (int64_t)1 << 27;
+  if (const char* e = std::getenv("FDH_SETUP_PAIR_CHUNK")) kChunk = std::max(1024LL, std::atoll(e));  // testing
   for (int l = 0; l <= maxl; ++l) {
     LevelBlocks& B = P.blocks[l];
-    B.lp_t = down(lpt[l], nlp[l]);
-    B.lp_s = down(lps[l], nlp[l]);
-    B.lp_key = down(lpk[l], nlp[l]);
+    if (!shard || nlp[l] == 0) {
+      B.lp_t = down(lpt[l], nlp[l]);
+      B.lp_s = down(lps[l], nlp[l]);
+      B.lp_key = down(lpk[l], nlp[l]);
+      continue;
+    }
+    std::vector<uint8_t> needh(P.t_needed[l].begin(), P.t_needed[l].end());
+    uint8_t* need = D.up(needh);
+    int64_t* f = D.alloc<int64_t>(std::min(nlp[l], kChunk));
+    for (int64_t c0 = 0; c0 < nlp[l]; c0 += kChunk) {
+      const int64_t nc = std::min(kChunk, nlp[l] - c0);
+      k_needed_flags<<<nblocks(nc), 256>>>(nc, lpt[l] + c0, need, f);
+      const int64_t k = scan_excl(D, f, nc);
+      int32_t* ot = D.alloc<int32_t>(k);
+      int32_t* os = D.alloc<int32_t>(k);
+      int32_t* ok = D.alloc<int32_t>(k);
+      k_needed_emit<<<nblocks(nc), 256>>>(nc, lpt[l] + c0, lps[l] + c0, lpk[l] + c0, need, f, ot, os, ok);
+      SCK(cudaGetLastError());
+      const auto ht = down(ot, k), hs = down(os, k), hk = down(ok, k);
+      B.lp_t.insert(B.lp_t.end(), ht.begin(), ht.end());
+      B.lp_s.insert(B.lp_s.end(), hs.begin(), hs.end());
+      B.lp_key.insert(B.lp_key.end(), hk.begin(), hk.end());
+      for (void* p : {(void*)ot, (void*)os, (void*)ok}) D.release(p);
+    }
+    D.release(f);
+    D.release(need);
   }
   SCK(cudaDeviceSynchronize());
 }

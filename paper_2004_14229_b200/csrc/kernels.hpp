@@ -77,6 +77,8 @@ struct M2LI8Args {
   int nkq = 0, n_pad = 0, fkeys = 0;
   int n_tile = 0;        // ticket chains: one per tile and M-block group (m = 6: 2 groups)
   int64_t key_base = 0;  // first key of the Wq buffer (on-the-fly segments)
+  int nrhs = 1;          // moment scales per (rhs, level): lvmax_v[rhs * kMaxLevels + level];
+                         // tile column c = (slot, rhs) with rhs = c % nrhs
 };
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)

@@ -499,7 +499,7 @@ void build_m2l(Plan& P) {
   // within a slot, so the result is deterministic)
   int64_t npairs = 0;
   for (auto& B : P.blocks) npairs += (int64_t)B.lp_t.size();
-  P.n_c = npairs;
+  if (!P.prm.gpu_structure) P.n_c = npairs;  // GPU partition: the full |L+| (shards hold a part)
   std::unique_ptr<std::atomic<int64_t>[]> cnt(new std::atomic<int64_t>[T.nslots + 1]);
   for (int64_t i = 0; i <= T.nslots; ++i) cnt[i].store(0, std::memory_order_relaxed);
   for (int l = 0; l < (int)P.blocks.size(); ++l) {
@@ -824,6 +824,91 @@ void dir_vec(int level, int lhf, int idx, double out[3]) {
   for (int i = 0; i < 3; ++i) out[i] = (1.0 / nn) * p[i];
 }
 
+// Ownership of target leaves for sharded runs: leaves in
+// Morton order, split into `world` contiguous ranges of equal estimated cost,
+// cost(leaf) = sum over the leaf and its ancestors a of
+//   (8 n^2 * #L+(a) + 24 * near-field pairs(a)) * points(leaf) / points(a);
+// then the ancestor closure of the owned leaves (t_needed).  #L+ per target node
+// comes from P.lp_count when the partition was built on the GPU (the L+ lists are
+// then compacted to t_needed on the device before they reach the host), else from
+// the host lists.
+void compute_ownership(Plan& P) {
+  const PlanParams& prm = P.prm;
+  const TreePlan& T = P.T;
+  const int D = T.depth;
+  std::vector<std::vector<double>> own(D + 1);
+  for (int l = 0; l <= D; ++l) own[l].assign(T.lv[l].size(), 0.0);
+  const double fl_m2l = 8.0 * P.n * P.n;
+  for (int l = 0; l < (int)P.blocks.size(); ++l) {
+    const LevelBlocks& B = P.blocks[l];
+    if (l < (int)P.lp_count.size() && !P.lp_count[l].empty()) {
+      for (size_t i = 0; i < P.lp_count[l].size(); ++i) own[l][i] += fl_m2l * P.lp_count[l][i];
+    } else {
+      for (size_t b = 0; b < B.lp_t.size(); ++b) own[l][B.lp_t[b]] += fl_m2l;
+    }
+    for (size_t b = 0; b < B.lm_t.size(); ++b)
+      own[l][B.lm_t[b]] += 24.0 * (double)(T.lv[l].end[B.lm_t[b]] - T.lv[l].begin[B.lm_t[b]]) *
+                           (double)(P.S.lv[l].end[B.lm_s[b]] - P.S.lv[l].begin[B.lm_s[b]]);
+  }
+  // push ancestor cost down by point share: dens[l][i] = cost per point inherited
+  std::vector<std::vector<double>> dens(D + 1);
+  for (int l = 0; l <= D; ++l) {
+    dens[l].assign(T.lv[l].size(), 0.0);
+    for (size_t i = 0; i < T.lv[l].size(); ++i) {
+      const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
+      const double inh = l > 0 ? dens[l - 1][T.lv[l].parent[i]] : 0.0;
+      dens[l][i] = inh + own[l][i] / pts;
+    }
+  }
+  // Morton key of the leaf's lower corner at the deepest level: 3 bits per level,
+  // 128-bit so that any depth up to the cap keeps the spatial order
+  struct LeafRef { unsigned __int128 key; int64_t id; double c; };
+  std::vector<LeafRef> lr;
+  int64_t id = 0;
+  for (int l = 0; l <= D; ++l)
+    for (size_t i = 0; i < T.lv[l].size(); ++i) {
+      if (!T.lv[l].leaf[i]) continue;
+      unsigned __int128 k = 0;
+      const int64_t ci = T.lv[l].ci[i] << (D - l), cj = T.lv[l].cj[i] << (D - l), ck = T.lv[l].ck[i] << (D - l);
+      for (int b = D - 1; b >= 0; --b)
+        k = (k << 3) | (unsigned)((((ci >> b) & 1) << 2) | (((cj >> b) & 1) << 1) | ((ck >> b) & 1));
+      const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
+      lr.push_back({k, id++, dens[l][i] * pts + 1.0});
+    }
+  std::sort(lr.begin(), lr.end(), [](const LeafRef& a, const LeafRef& b) { return a.key < b.key; });
+  double tot = 0;
+  for (auto& r : lr) tot += r.c;
+  P.t_leaf_owned.assign(id, 0);
+  P.shard_cost = 0.0;
+  double acc = 0;
+  for (auto& r : lr) {
+    const double mid = acc + 0.5 * r.c;
+    const int owner = std::min(prm.world - 1, (int)(mid / tot * prm.world));
+    if (owner == prm.rank) {
+      P.t_leaf_owned[r.id] = 1;
+      P.shard_cost += r.c;
+    }
+    acc += r.c;
+  }
+  P.total_cost = tot;
+  // ancestor closure of the owned leaves (leaf ids in (level, Morton) order)
+  P.t_needed.assign(P.T.depth + 1, {});
+  for (int l = 0; l <= P.T.depth; ++l) P.t_needed[l].assign(P.T.lv[l].size(), 0);
+  int64_t lid = 0;
+  for (int l = 0; l <= P.T.depth; ++l)
+    for (size_t i = 0; i < P.T.lv[l].size(); ++i) {
+      if (!P.T.lv[l].leaf[i]) continue;
+      if (P.t_leaf_owned[lid++]) {
+        int32_t nid = (int32_t)i;
+        for (int ll = l; ll >= 0 && !P.t_needed[ll][nid]; --ll) {
+          P.t_needed[ll][nid] = 1;
+          nid = P.T.lv[ll].parent[nid];
+          if (nid < 0) break;
+        }
+      }
+    }
+}
+
 void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
                 const double* sy, const double* sz, int64_t ns, const double lo[3], const double hi[3],
                 const PlanParams& prm) {
@@ -893,81 +978,7 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
         }
     }
   }
-  // ownership of target leaves for sharded runs: leaves in
-  // Morton order, split into `world` contiguous ranges of equal estimated cost,
-  // cost(leaf) = sum over the leaf and its ancestors a of
-  //   (8 n^2 * #L+(a) + 24 * near-field pairs(a)) * points(leaf) / points(a).
-  if (prm.world > 1) {
-    const TreePlan& T = P.T;
-    const int D = T.depth;
-    std::vector<std::vector<double>> own(D + 1);
-    for (int l = 0; l <= D; ++l) own[l].assign(T.lv[l].size(), 0.0);
-    const double fl_m2l = 8.0 * P.n * P.n;
-    for (int l = 0; l < (int)P.blocks.size(); ++l) {
-      const LevelBlocks& B = P.blocks[l];
-      for (size_t b = 0; b < B.lp_t.size(); ++b) own[l][B.lp_t[b]] += fl_m2l;
-      for (size_t b = 0; b < B.lm_t.size(); ++b)
-        own[l][B.lm_t[b]] += 24.0 * (double)(T.lv[l].end[B.lm_t[b]] - T.lv[l].begin[B.lm_t[b]]) *
-                             (double)(P.S.lv[l].end[B.lm_s[b]] - P.S.lv[l].begin[B.lm_s[b]]);
-    }
-    // push ancestor cost down by point share: dens[l][i] = cost per point inherited
-    std::vector<std::vector<double>> dens(D + 1);
-    for (int l = 0; l <= D; ++l) {
-      dens[l].assign(T.lv[l].size(), 0.0);
-      for (size_t i = 0; i < T.lv[l].size(); ++i) {
-        const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
-        const double inh = l > 0 ? dens[l - 1][T.lv[l].parent[i]] : 0.0;
-        dens[l][i] = inh + own[l][i] / pts;
-      }
-    }
-    struct LeafRef { uint64_t key; int64_t id; double c; };
-    std::vector<LeafRef> lr;
-    int64_t id = 0;
-    for (int l = 0; l <= D; ++l)
-      for (size_t i = 0; i < T.lv[l].size(); ++i) {
-        if (!T.lv[l].leaf[i]) continue;
-        uint64_t k = 0;
-        const int64_t ci = T.lv[l].ci[i] << (D - l), cj = T.lv[l].cj[i] << (D - l), ck = T.lv[l].ck[i] << (D - l);
-        for (int b = D - 1; b >= 0; --b)
-          k = (k << 3) | (((ci >> b) & 1) << 2) | (((cj >> b) & 1) << 1) | ((ck >> b) & 1);
-        const double pts = (double)(T.lv[l].end[i] - T.lv[l].begin[i]);
-        lr.push_back({k, id++, dens[l][i] * pts + 1.0});
-      }
-    std::sort(lr.begin(), lr.end(), [](const LeafRef& a, const LeafRef& b) { return a.key < b.key; });
-    double tot = 0;
-    for (auto& r : lr) tot += r.c;
-    P.t_leaf_owned.assign(id, 0);
-    P.shard_cost = 0.0;
-    double acc = 0;
-    for (auto& r : lr) {
-      const double mid = acc + 0.5 * r.c;
-      const int owner = std::min(prm.world - 1, (int)(mid / tot * prm.world));
-      if (owner == prm.rank) {
-        P.t_leaf_owned[r.id] = 1;
-        P.shard_cost += r.c;
-      }
-      acc += r.c;
-    }
-    P.total_cost = tot;
-  }
-  if (!P.t_leaf_owned.empty()) {
-    // ancestor closure of the owned leaves (leaf ids in (level, Morton) order)
-    P.t_needed.assign(P.T.depth + 1, {});
-    for (int l = 0; l <= P.T.depth; ++l) P.t_needed[l].assign(P.T.lv[l].size(), 0);
-    int64_t lid = 0;
-    for (int l = 0; l <= P.T.depth; ++l)
-      for (size_t i = 0; i < P.T.lv[l].size(); ++i) {
-        if (!P.T.lv[l].leaf[i]) continue;
-        if (P.t_leaf_owned[lid++]) {
-          int32_t id = (int32_t)i;
-          for (int ll = l; ll >= 0 && !P.t_needed[ll][id]; --ll) {
-            P.t_needed[ll][id] = 1;
-            id = P.T.lv[ll].parent[id];
-            if (id < 0) break;
-          }
-        }
-      }
-  }
+  if (prm.world > 1 && P.t_leaf_owned.empty()) compute_ownership(P);
   auto tick = [&](const char* what, std::chrono::steady_clock::time_point& ts) {
     const auto now = std::chrono::steady_clock::now();
     if (std::getenv("FDH_DEBUG_SETUP"))
@@ -1139,8 +1150,10 @@ void structure_digest(const Plan& P, uint64_t out[6]) {
     const LevelNodes& LT = P.T.lv[l];
     const LevelNodes& LS = P.S.lv[l];
     uint64_t a = 0;
+    // (the digest of the full list is taken on the device when it was built there)
+    const int64_t nlp = P.lplus_digest_dev ? 0 : (int64_t)B.lp_t.size();
 #pragma omp parallel for reduction(+ : a)
-    for (int64_t b = 0; b < (int64_t)B.lp_t.size(); ++b) {
+    for (int64_t b = 0; b < nlp; ++b) {
       const int64_t r[8] = {l, LT.ci[B.lp_t[b]], LT.cj[B.lp_t[b]], LT.ck[B.lp_t[b]], LS.ci[B.lp_s[b]], LS.cj[B.lp_s[b]],
                             LS.ck[B.lp_s[b]], P.key_dir[B.lp_key[b]]};
       a += row_hash(r, 8);
@@ -1152,7 +1165,7 @@ void structure_digest(const Plan& P, uint64_t out[6]) {
       lm += row_hash(r, 8);
     }
   }
-  out[2] = lp;
+  out[2] = P.lplus_digest_dev ? P.lplus_digest : lp;
   out[3] = lm;
 }
 

@@ -130,6 +130,11 @@ struct Plan {
   std::vector<std::vector<uint8_t>> t_needed;  // [level][node]: owned leaf or ancestor of one
   double shard_cost = 0.0, total_cost = 0.0;     // estimated flops of this shard / of all targets
   double nf_max_dist = 0.0;  // upper bound of |x_j - y_k| over the near-field pairs
+  // GPU partition (k_setup.cu): #L+ per target node per level (shard cost model),
+  // the L+ digest of the FULL list (the host keeps only the t_needed part on shards)
+  std::vector<std::vector<int32_t>> lp_count;
+  uint64_t lplus_digest = 0;
+  bool lplus_digest_dev = false;
 
   // statistics
   int64_t n_c = 0, n_sc = 0, m_d = 0, n_le = 0, n_lminus = 0;
@@ -150,6 +155,8 @@ int64_t export_lminus(const Plan& P, int64_t* rows);
 int64_t export_dirsets(const Plan& P, int which, int64_t* rows);
 int64_t export_owned_leaves(const Plan& P, int64_t* rows);
 void structure_digest(const Plan& P, uint64_t out[6]);
+// shard ownership (cost-balanced Morton ranges of target leaves) + t_needed
+void compute_ownership(Plan& P);
 
 // direction conventions
 int num_dirs(int level, int lhf);
