@@ -99,7 +99,11 @@ typedef struct fdh_stats {
 /* Setup: both cluster trees (Alg. 1), the direction table
  * (Alg. 3), the block tree with L+/L- and D/D^ sets (Alg. 2, Def. 4), the
  * coupling matrices of every (level, offset) key (Eq. 9), device buffers.
- * n_gpus must be 1 (multi-GPU runs one operator per rank, see fdh_create_shard). */
+ * n_gpus > 1: one process drives devices 0 .. n_gpus-1, device g holding the
+ * target-leaf shard g of n_gpus (fdh_create_shard, set up concurrently); an
+ * apply broadcasts x from device 0 and reduces y onto device 0 over NCCL
+ * (libnccl.so.2 loaded at run time).  fdh_apply_device on such an operator takes
+ * device-0 pointers and a device-0 stream; exports describe device 0's shard. */
 int fdh_create(const double* tx, const double* ty, const double* tz, int64_t nt,
                const double* sx, const double* sy, const double* sz, int64_t ns,
                const double root_lo[3], const double root_hi[3], double kappa, int n_max, int m,

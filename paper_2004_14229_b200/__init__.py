@@ -124,7 +124,7 @@ class DirectionalOperator:
     """
 
     def __init__(self, targets, sources, root_lo, root_hi, kappa, n_max=64, m=4, eta2=1.0, l_hf=LHF_DEFAULT,
-                 depth_cap=30, zero_diagonal=False, rank=0, world=1, plan_only=False, nrhs=1):
+                 depth_cap=30, zero_diagonal=False, rank=0, world=1, plan_only=False, nrhs=1, n_gpus=1):
         L = lib()
         self._keep = [_f64(a) for a in (*targets, *sources)]
         tx, ty, tz, sx, sy, sz = self._keep
@@ -142,7 +142,9 @@ class DirectionalOperator:
         elif world > 1:
             _chk(L.fdh_create_shard(*args, int(rank), int(world), C.byref(h)))
         else:
-            _chk(L.fdh_create(*args, 1, C.byref(h)))
+            # n_gpus > 1: one process drives n_gpus devices (shard g on device g, NCCL
+            # reduce of y onto device 0 inside the library)
+            _chk(L.fdh_create(*args, int(n_gpus), C.byref(h)))
         self.h = h
         self.nt, self.ns = len(tx), len(sx)
 

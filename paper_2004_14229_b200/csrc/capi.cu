@@ -1,8 +1,11 @@
 // capi.cu -- the C-ABI (include/fdhelm_c.h): operator setup, device residency
 // and the Alg. 4 apply sequence on one CUDA stream.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is resolved at run time (dlopen), see nccl()
 
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -25,6 +28,43 @@ struct CudaErr {
   do {                                                                                             \
     cudaError_t e_ = (x);                                                                          \
     if (e_ != cudaSuccess) throw CudaErr{std::string(#x) + ": " + cudaGetErrorString(e_)};         \
+  } while (0)
+
+// NCCL, loaded on first multi-GPU use: the process's libnccl.so.2 if one is
+// already loaded (e.g. by torch), else the system one -- no link-time dependency
+struct NcclApi {
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi* nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.CommInitAll = (decltype(api.CommInitAll))dlsym(h, "ncclCommInitAll");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+      api.Reduce = (decltype(api.Reduce))dlsym(h, "ncclReduce");
+      api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+      api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    }
+  }
+  return api.CommInitAll && api.Reduce && api.Broadcast && api.GroupStart && api.GroupEnd ? &api : nullptr;
+}
+#define NK(x)                                                                                      \
+  do {                                                                                             \
+    ncclResult_t r_ = (x);                                                                         \
+    if (r_ != ncclSuccess) throw CudaErr{std::string(#x) + ": " + nccl()->GetErrorString(r_)};     \
   } while (0)
 
 struct LevelDev {
@@ -69,6 +109,7 @@ struct fdh_op {
           *tile_nitem = nullptr, *tile_tslot = nullptr;
   double* tile_acc = nullptr;
   int* ticket = nullptr;
+  int* counter = nullptr;  // int8 M2L item-claim counters: passes x segments
   int64_t *item_k0 = nullptr, *item_k1 = nullptr;
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
@@ -124,8 +165,19 @@ struct fdh_op {
   const void* gy = nullptr;
   cudaStream_t gst = nullptr;
   int64_t graph_replays = 0;
+  // multi-GPU operator (fdh_create with n_gpus > 1): one target-leaf shard per
+  // device (rank g of n_gpus on device g), y reduced to device 0 over NCCL
+  std::vector<fdh_op*> parts;
+  std::vector<ncclComm_t> comms;
 
   ~fdh_op() {
+    for (size_t g = 0; g < parts.size(); ++g) {
+      cudaSetDevice(parts[g]->device);
+      delete parts[g];
+    }
+    if (!parts.empty()) cudaSetDevice(0);  // the group's own buffers live on device 0
+    for (ncclComm_t c : comms)
+      if (c && nccl()) nccl()->CommDestroy(c);
     if (st) cudaStreamSynchronize(st);
     if (gexec) cudaGraphExecDestroy(gexec);
     for (void* p : allocs) cudaFree(p);
@@ -318,7 +370,7 @@ void setup_device(fdh_op* o) {
   o->mom = o->alloc<double>((size_t)(R * P.S.nslots * np2));  // [rhs][slot][Re | Im]
   o->loc = o->alloc<double>((size_t)(R * P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
-  o->ticket = o->alloc<int>((size_t)std::max(2 * o->n_tile, 1));  // int8 m = 6: one chain per M-block group
+  o->ticket = o->alloc<int>((size_t)std::max(3 * o->n_tile, 1));  // int8: one chain per M-block pass (<= 3)
   o->q = o->alloc<double2>((size_t)(R * o->ns));
   o->q4 = o->alloc<double2>((size_t)(R * o->ns));
   {
@@ -387,15 +439,16 @@ void setup_device(fdh_op* o) {
       for (int pass = 0; pass < 2; ++pass)
         for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
           launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
-                             o->key_dir, pass, o->lvmax_w, o->Wq, P.n, o->nkq);
+                             o->key_dir, pass, o->lvmax_w, o->Wq, P.n, o->nkq, m2l_i8_wgroup(P.n, P.prm.tile));
     } else {
       for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)  // scales only
         launch_coupling_i8(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d,
-                           o->key_dir, 0, o->lvmax_w, nullptr, P.n, o->nkq);
+                           o->key_dir, 0, o->lvmax_w, nullptr, P.n, o->nkq, m2l_i8_wgroup(P.n, P.prm.tile));
       const int64_t slot_keys = make_segments(wkq);
       o->Wq = o->alloc<int8_t>((size_t)(2 * slot_keys * wkq));
       CK(cudaMemsetAsync(o->Wq, 0, (size_t)(2 * slot_keys * wkq), o->st));  // padding rows / K stay zero
     }
+    o->counter = o->alloc<int>((size_t)(m2l_i8_passes(P.n, P.prm.tile) * std::max<size_t>(1, o->segs.size())));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(o->st));
     return;
@@ -413,6 +466,7 @@ void setup_device(fdh_op* o) {
     const int64_t slot_keys = make_segments(8 * wkey);
     o->W = o->alloc<double>((size_t)(2 * slot_keys * wkey));
   }
+  o->counter = o->alloc<int>(std::max<size_t>(1, o->segs.size()));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(o->st));
   if (o->n_item > 0 && P.prm.m > 6)
@@ -475,7 +529,9 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   }
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(R * lstr), st));
   if (o->n_item > 0 && o->i8) {
-    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(2 * o->n_tile), st));
+    const int npass = m2l_i8_passes(n, P.prm.tile);
+    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(npass * o->n_tile), st));
+    CK(cudaMemsetAsync(o->counter, 0, sizeof(int) * (size_t)(npass * std::max<size_t>(1, o->segs.size())), st));
     launch_mom_quant(st, o->mom, o->s_slot_level, P.S.nslots, n, np, o->nkq, o->lvmax_v, o->Mq, R);
     M2LI8Args a;
     a.n_item = o->n_item;
@@ -503,7 +559,8 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.fkeys = P.prm.m2l_fkeys;
     a.n_tile = o->n_tile;
     a.nrhs = R;
-    const int ng = m2l_i8_groups(n);
+    a.counter = o->counter;
+    const int ng = npass;
     rec(o, FDH_NPHASES + 1, st);
     if (o->w_resident) {
       if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
@@ -514,12 +571,13 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
         const auto& S = o->segs[sg];
         int8_t* slot = o->Wq + (int64_t)(sg & 1) * o->w_slot_keys * wkq;
         launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
-                           o->lvmax_w, slot, n, o->nkq, S.key0);
+                           o->lvmax_w, slot, n, o->nkq, m2l_i8_wgroup(n, P.prm.tile), S.key0);
         M2LI8Args b = a;
         b.item0 = S.item0;
         b.n_item = S.item1 - S.item0;
         b.Wq = slot;
         b.key_base = S.key0;
+        b.counter = o->counter + sg * npass;
         if (launch_m2l_i8(st, n, P.prm.tile, b) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
         L += 1 + ng;
       }
@@ -528,6 +586,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     rec(o, FDH_NPHASES + 2, st);
   } else if (o->n_item > 0) {
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
+    CK(cudaMemsetAsync(o->counter, 0, sizeof(int) * std::max<size_t>(1, o->segs.size()), st));
     M2LArgs a;
     a.n_item = o->n_item;
     a.item_tile = o->item_tile;
@@ -547,6 +606,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.ticket = o->ticket;
     a.loc = o->loc;
     a.err = o->flag;
+    a.counter = o->counter;
     rec(o, FDH_NPHASES + 1, st);
     if (o->w_resident) {
       if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, a) != 0)
@@ -562,6 +622,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
         b.n_item = S.item1 - S.item0;
         b.W = slot;
         b.key_base = S.key0;
+        b.counter = o->counter + sg;
         if (launch_m2l_gemm(st, np, P.n_k, P.prm.tile, b) != 0)
           throw PlanError{4, "no M2L kernel for this n_pad / tile"};
         L += 2;
@@ -764,6 +825,8 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     if (want_i8) {
       prm.m2l_impl = 1;
       prm.tile = nbox <= 128 ? 32 : 16;
+      if (const char* tt = std::getenv("FDH_I8_TILE"))  // 32: one M-block per pass for m = 5, 6 (N up to 448)
+        prm.tile = std::atoi(tt) == 32 ? 32 : prm.tile;
       prm.m2l_fkeys = m2l_i8_fkeys((nbox + 15) / 16 * 16);
       if (const char* fk = std::getenv("FDH_M2L_FKEYS"))  // testing knob: shorter items (more chaining)
         prm.m2l_fkeys = std::max(1, std::min(prm.m2l_fkeys, std::atoi(fk)));
@@ -796,6 +859,59 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
   return FDH_OK;
 }
 
+// Multi-GPU apply: x on device 0 (xd) is broadcast to every shard over NCCL,
+// every device applies its shard (its own stream, CUDA-graph replay), the shard
+// outputs are summed into yd on device 0 by an NCCL reduce.  All on the shards'
+// streams; the caller's stream on device 0 is joined by events.
+void group_apply(fdh_op* G, const double2* xd, double2* yd, cudaStream_t st0) {
+  const int N = (int)G->parts.size();
+  fdh_op* p0 = G->parts[0];
+  if (st0 && st0 != p0->st) {  // order after the caller's work on its stream
+    CK(cudaSetDevice(p0->device));
+    CK(cudaEventRecord(p0->ev_q, st0));
+    CK(cudaStreamWaitEvent(p0->st, p0->ev_q, 0));
+  }
+  NK(nccl()->GroupStart());
+  for (int g = 0; g < N; ++g) {
+    fdh_op* p = G->parts[g];
+    CK(cudaSetDevice(p->device));
+    NK(nccl()->Broadcast(xd, g == 0 ? (void*)xd : (void*)p->xin, 2 * (size_t)p->ns, ncclDouble, 0, G->comms[g],
+                         p->st));
+  }
+  NK(nccl()->GroupEnd());
+  for (int g = 0; g < N; ++g) {
+    fdh_op* p = G->parts[g];
+    CK(cudaSetDevice(p->device));
+    apply_graph(p, g == 0 ? xd : p->xin, p->yout, p->st);
+  }
+  NK(nccl()->GroupStart());
+  for (int g = 0; g < N; ++g) {
+    fdh_op* p = G->parts[g];
+    CK(cudaSetDevice(p->device));
+    NK(nccl()->Reduce(p->yout, yd, 2 * (size_t)p->nt, ncclDouble, ncclSum, 0, G->comms[g], p->st));
+  }
+  NK(nccl()->GroupEnd());
+  if (st0 && st0 != p0->st) {
+    CK(cudaSetDevice(p0->device));
+    CK(cudaEventRecord(p0->ev_nf, p0->st));
+    CK(cudaStreamWaitEvent(st0, p0->ev_nf, 0));
+  }
+  CK(cudaSetDevice(p0->device));
+}
+
+void group_sync(fdh_op* G, int* flag_or) {
+  for (fdh_op* p : G->parts) {
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->st));
+    int f = 0;
+    CK(cudaMemcpy(&f, p->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(p->flag, 0, sizeof(int)));
+    collect_times(p);
+    *flag_or |= f;
+  }
+  CK(cudaSetDevice(G->parts[0]->device));
+}
+
 }  // namespace
 
 extern "C" {
@@ -806,10 +922,65 @@ const char* fdh_version(void) { return "fdhelm-b200 0.2 (sm_100a; M2L: tcgen05 i
 int fdh_create(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx, const double* sy,
                const double* sz, int64_t ns, const double root_lo[3], const double root_hi[3], double kappa, int n_max,
                int m, double eta2, int l_hf, int depth_cap, int zero_diagonal, int n_gpus, fdh_op** out) {
-  if (n_gpus != 1)
-    return fail(FDH_ERR_UNSUPPORTED, "n_gpus must be 1: run one operator per rank via fdh_create_shard");
-  return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
-                       zero_diagonal, 0, 1, out);
+  if (!out) return fail(FDH_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_gpus < 1) return fail(FDH_ERR_ARG, "n_gpus must be >= 1");
+  const char* grp = std::getenv("FDH_GROUP");  // testing knob: the multi-GPU path with n_gpus = 1
+  if (n_gpus == 1 && !(grp && grp[0] == '1'))
+    return create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf, depth_cap,
+                         zero_diagonal, 0, 1, out);
+  // one process, n_gpus devices (SURVEY.md 8(b) "internally multi-GPU"): rank g of
+  // n_gpus (cost-balanced target-leaf shard, fdh_create_shard) on device g, the
+  // shards set up concurrently by one host thread each; y is reduced over NCCL
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < n_gpus)
+    return fail(FDH_ERR_UNSUPPORTED, "n_gpus = " + std::to_string(n_gpus) + " needs that many CUDA devices, found " +
+                                         std::to_string(ndev));
+  if (!nccl()) return fail(FDH_ERR_UNSUPPORTED, "n_gpus > 1 needs libnccl.so.2 (not found)");
+  fdh_op* g = new fdh_op;
+  g->parts.assign(n_gpus, nullptr);
+  g->nt = nt;
+  g->ns = ns;
+  std::vector<int> rc(n_gpus, FDH_OK);
+  std::vector<std::string> msg(n_gpus);
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::thread> th;
+    for (int d = 0; d < n_gpus; ++d)
+      th.emplace_back([&, d] {
+        if (cudaSetDevice(d) != cudaSuccess) {
+          rc[d] = FDH_ERR_CUDA;
+          msg[d] = "cudaSetDevice failed";
+          return;
+        }
+        rc[d] = create_common(tx, ty, tz, nt, sx, sy, sz, ns, root_lo, root_hi, kappa, n_max, m, eta2, l_hf,
+                              depth_cap, zero_diagonal, d, n_gpus, &g->parts[d]);
+        if (rc[d] != FDH_OK) msg[d] = g_err;
+      });
+    for (auto& t : th) t.join();
+  }
+  for (int d = 0; d < n_gpus; ++d)
+    if (rc[d] != FDH_OK) {
+      const int r = rc[d];
+      const std::string m = "device " + std::to_string(d) + ": " + msg[d];
+      delete g;
+      return fail(r, m);
+    }
+  const int r = guard([&] {
+    std::vector<int> devs(n_gpus);
+    for (int d = 0; d < n_gpus; ++d) devs[d] = d;
+    g->comms.assign(n_gpus, nullptr);
+    NK(nccl()->CommInitAll(g->comms.data(), n_gpus, devs.data()));
+    CK(cudaSetDevice(0));
+    g->yout = g->alloc<double2>((size_t)nt);  // the reduced y on device 0
+  });
+  if (r != FDH_OK) {
+    delete g;
+    return r;
+  }
+  g->stats.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = g;
+  return FDH_OK;
 }
 
 int fdh_create_shard(const double* tx, const double* ty, const double* tz, int64_t nt, const double* sx,
@@ -841,6 +1012,23 @@ void fdh_destroy(fdh_op* op) { delete op; }
 int fdh_apply_multi(fdh_op* o, const double* x, int64_t k, double* y) {
   if (!o || !x || !y) return fail(FDH_ERR_ARG, "NULL argument");
   if (k < 1) return fail(FDH_ERR_ARG, "need at least one right-hand side");
+  if (!o->parts.empty()) {
+    return guard([&] {
+      fdh_op* p0 = o->parts[0];
+      for (int64_t b = 0; b < k; ++b) {
+        CK(cudaSetDevice(p0->device));
+        CK(cudaMemcpyAsync(p0->xin, x + 2 * b * o->ns, sizeof(double2) * (size_t)o->ns, cudaMemcpyHostToDevice,
+                           p0->st));
+        group_apply(o, p0->xin, o->yout, nullptr);
+        CK(cudaSetDevice(p0->device));
+        CK(cudaMemcpyAsync(y + 2 * b * o->nt, o->yout, sizeof(double2) * (size_t)o->nt, cudaMemcpyDeviceToHost,
+                           p0->st));
+        int flag = 0;
+        group_sync(o, &flag);
+        if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+      }
+    });
+  }
   if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
   return guard([&] {
     CK(cudaSetDevice(o->device));
@@ -859,7 +1047,6 @@ int fdh_apply_multi(fdh_op* o, const double* x, int64_t k, double* y) {
       CK(cudaMemcpyAsync(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost, o->st));
       CK(cudaStreamSynchronize(o->st));
       collect_times(o);
-      if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
       if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
     }
   });
@@ -869,6 +1056,11 @@ int fdh_apply(fdh_op* o, const double* x, double* y) { return fdh_apply_multi(o,
 
 int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream) {
   if (!o || !x_dev || !y_dev) return fail(FDH_ERR_ARG, "NULL argument");
+  if (!o->parts.empty())  // multi-GPU: x_dev / y_dev / stream on device 0
+    return guard([&] {
+      group_apply(o, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev),
+                  static_cast<cudaStream_t>(stream));
+    });
   if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
   return guard([&] {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : o->st;
@@ -878,6 +1070,12 @@ int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream
 
 int fdh_sync(fdh_op* o) {
   if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  if (!o->parts.empty())
+    return guard([&] {
+      int flag = 0;
+      group_sync(o, &flag);
+      if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+    });
   if (!o->st) return FDH_OK;
   return guard([&] {
     CK(cudaSetDevice(o->device));
@@ -886,15 +1084,22 @@ int fdh_sync(fdh_op* o) {
     int flag = 0;
     CK(cudaMemcpy(&flag, o->flag, sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemset(o->flag, 0, sizeof(int)));
-    if (flag & 2) throw PlanError{FDH_ERR_CUDA, "M2L item chain timed out (accumulation order not guaranteed)"};
     if (flag & 1) throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
   });
 }
 
-void* fdh_stream(fdh_op* o) { return o ? static_cast<void*>(o->st) : nullptr; }
+void* fdh_stream(fdh_op* o) {
+  if (o && !o->parts.empty()) return static_cast<void*>(o->parts[0]->st);
+  return o ? static_cast<void*>(o->st) : nullptr;
+}
 
 int fdh_set_timing(fdh_op* o, int enable) {
   if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  for (fdh_op* p : o->parts) {
+    cudaSetDevice(p->device);
+    if (const int rc = fdh_set_timing(p, enable)) return rc;
+  }
+  if (!o->parts.empty()) cudaSetDevice(0);
   return guard([&] {
     if (o->st) {
       CK(cudaStreamSynchronize(o->st));
@@ -911,6 +1116,29 @@ int fdh_set_timing(fdh_op* o, int enable) {
 
 int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   if (!o || !s) return fail(FDH_ERR_ARG, "NULL argument");
+  if (!o->parts.empty()) {
+    // multi-GPU: structure counters of the (full) partition from device 0's shard,
+    // times = max over the devices, bytes / launches summed
+    fdh_stats t{};
+    for (size_t g = 0; g < o->parts.size(); ++g) {
+      cudaSetDevice(o->parts[g]->device);
+      if (const int rc = fdh_get_stats(o->parts[g], g == 0 ? s : &t)) return rc;
+      if (g == 0) continue;
+      s->apply_ms = std::max(s->apply_ms, t.apply_ms);
+      s->apply_ms_sum = std::max(s->apply_ms_sum, t.apply_ms_sum);
+      for (int ph = 0; ph < FDH_NPHASES; ++ph) s->phase_ms[ph] = std::max(s->phase_ms[ph], t.phase_ms[ph]);
+      s->m2l_gemm_ms = std::max(s->m2l_gemm_ms, t.m2l_gemm_ms);
+      s->bytes_stored += t.bytes_stored;
+      s->gpu_launches += t.gpu_launches;
+      s->m2l_i8_ops += t.m2l_i8_ops;
+      s->m2l_tiles += t.m2l_tiles;
+      s->m2l_items += t.m2l_items;
+    }
+    cudaSetDevice(0);
+    s->setup_ms = o->stats.setup_ms;
+    s->shard_cost = s->total_cost;
+    return FDH_OK;
+  }
   fdh_op* m = const_cast<fdh_op*>(o);
   if (m->st) {
     cudaStreamSynchronize(m->st);
@@ -983,23 +1211,40 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   return FDH_OK;
 }
 
+// introspection of a multi-GPU operator: device 0's shard (full trees, L-, D/D^;
+// L+ and owned leaves of that shard)
+static const fdh_op* prim(const fdh_op* o) { return (o && !o->parts.empty()) ? o->parts[0] : o; }
+
 int64_t fdh_export_tree(const fdh_op* o, int which, int64_t* rows) {
+  o = prim(o);
   return o ? export_tree(which == 0 ? o->P.T : o->P.S, rows) : -1;
 }
 int64_t fdh_export_perm(const fdh_op* o, int which, int64_t* perm) {
+  o = prim(o);
   return o ? export_perm(which == 0 ? o->P.T : o->P.S, perm) : -1;
 }
-int64_t fdh_export_lplus(const fdh_op* o, int64_t* rows) { return o ? export_lplus(o->P, rows) : -1; }
-int64_t fdh_export_lminus(const fdh_op* o, int64_t* rows) { return o ? export_lminus(o->P, rows) : -1; }
+int64_t fdh_export_lplus(const fdh_op* o, int64_t* rows) { return (o = prim(o)) ? export_lplus(o->P, rows) : -1; }
+int64_t fdh_export_lminus(const fdh_op* o, int64_t* rows) { return (o = prim(o)) ? export_lminus(o->P, rows) : -1; }
 int64_t fdh_export_dirsets(const fdh_op* o, int which, int64_t* rows) {
+  o = prim(o);
   return o ? export_dirsets(o->P, which, rows) : -1;
 }
 
-int64_t fdh_export_owned_leaves(const fdh_op* o, int64_t* rows) { return o ? export_owned_leaves(o->P, rows) : -1; }
+int64_t fdh_export_owned_leaves(const fdh_op* o, int64_t* rows) {
+  if (o && !o->parts.empty()) {  // every device's leaves
+    int64_t n = 0;
+    for (const fdh_op* p : o->parts) n += export_owned_leaves(p->P, nullptr);
+    if (!rows) return n;
+    int64_t off = 0;
+    for (const fdh_op* p : o->parts) off += export_owned_leaves(p->P, rows + 6 * off);
+    return off;
+  }
+  return o ? export_owned_leaves(o->P, rows) : -1;
+}
 
 int fdh_structure_digest(const fdh_op* o, uint64_t* out6) {
   if (!o || !out6) return fail(FDH_ERR_ARG, "NULL argument");
-  structure_digest(o->P, out6);
+  structure_digest(prim(o)->P, out6);
   return FDH_OK;
 }
 

@@ -387,6 +387,10 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // items of a tile are chained in chunk order by a ticket (earlier items are
 // dispatched first, so the wait is short and cannot deadlock); the last item
 // writes the locals.  Summation order is fixed -> bitwise deterministic.
+// Each CTA claims its item from an atomic counter when it starts (not by
+// blockIdx): an item's predecessor in its tile chain has a lower index, so it
+// was claimed by a CTA that is already running -- the chain always progresses,
+// whatever the dispatch order or concurrent kernels.
 template <int NPAD, int NK, int TT>
 __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD, NK, TT>::MINB) k_m2l_gemm(const int32_t* __restrict__ item_tile,
                                                    const int32_t* __restrict__ item_seq,
@@ -401,14 +405,17 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
                                                    const uint8_t* __restrict__ tile_same,
                                                    const double* __restrict__ W, const double* __restrict__ mom,
                                                    double* __restrict__ tile_acc, int* __restrict__ ticket,
-                                                   double* __restrict__ loc, int* __restrict__ err, int item0,
+                                                   double* __restrict__ loc, int* __restrict__ counter, int item0,
                                                    int64_t key_base) {
   using S = M2LShape<NPAD, NK, TT>;
   constexpr int MT = S::MT;
   extern __shared__ __align__(16) double smem[];
   double* sacc = smem + S::NBUF * S::STAGE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = item0 + (int)blockIdx.x;
+  __shared__ int s_item;
+  if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+  __syncthreads();
+  const int item = item0 + s_item;
   const int64_t k0 = item_k0[item], k1 = item_k1[item];
   // metadata window [w0, w0 + MK)
   int32_t* m_src = reinterpret_cast<int32_t*>(sacc + S::SR * S::SA);
@@ -510,16 +517,8 @@ __global__ void __launch_bounds__(M2LShape<NPAD, NK, TT>::THREADS, M2LShape<NPAD
   const int tile = item_tile[item], seq = item_seq[item], nit = tile_nitem[tile];
   double* A = tile_acc + (int64_t)tile * NPAD * 2 * TT;
   if (seq > 0) {
-    if (threadIdx.x == 0) {
-      long long spins = 0;
-      while (ld_acquire(ticket + tile) != seq) {
-        __nanosleep(200);
-        if (++spins > (1ll << 26)) {  // > ~10 s: report instead of hanging
-          atomicOr(err, 2);
-          break;
-        }
-      }
-    }
+    if (threadIdx.x == 0)
+      while (ld_acquire(ticket + tile) != seq) __nanosleep(100);
     __syncthreads();
   }
   const bool last = seq == nit - 1;
@@ -561,7 +560,7 @@ void run_gemm(cudaStream_t st, const M2LArgs& a) {
   k_m2l_gemm<NPAD, NK, TT><<<a.n_item, S::THREADS, S::SMEM, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1,
                                                               a.tile_nitem, a.tile_tslot, a.tile_keys, a.tile_src,
                                                               a.tile_cols, a.tile_cnt, a.tile_same, a.W, a.mom,
-                                                              a.tile_acc, a.ticket, a.loc, a.err, a.item0,
+                                                              a.tile_acc, a.ticket, a.loc, a.counter, a.item0,
                                                               a.key_base);
 }
 

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
                                                      const int64_t* __restrict__ key_d,
                                                      const int32_t* __restrict__ key_dir, int pass,
                                                      unsigned long long* __restrict__ lvmax, int8_t* __restrict__ Wq,
-                                                     int n, int nkq, int mb, int64_t key_base) {
+                                                     int n, int nkq, int mb, int gs, int64_t key_base) {
   __shared__ double tn[3][kMaxP], sn[3][kMaxP];
   __shared__ double red[8];
   const int64_t key = key0 + blockIdx.x;
@@ -211,15 +211,16 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
     int8_t dr[KS], di[KS];
     to_digits<KS>(re, ex, dr);
     to_digits<KS>(im, ex, di);
-    // M-block b belongs to group g = b / 2 (blocks {0, 1}, {2}); per (key, K chunk)
-    // the groups are stored one after the other, digit-major inside a group
+    // M-block b belongs to group g = b / gs (gs = 2: blocks {0, 1}, {2}; gs = 1: one
+    // block per group); per (key, K chunk) the groups are stored one after the
+    // other, digit-major inside a group -- the M-block passes of launch_m2l_i8
     const int b = j >> 7, rr = j & 127;
-    const int g = b >> 1, bg = b & 1, mbg = min(2, mb - 2 * g);
+    const int g = b / gs, bg = b % gs, mbg = min(gs, mb - gs * g);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int kk = h ? nkq + k : k;  // K index: [Re A | Im A]
       const int ch = kk / kKC, kin = kk % kKC;
-      int8_t* base = Wq + (((key - key_base) * nch + ch) * KS * mb + 2 * g * KS + bg) * (int64_t)kCore + core_off(rr, kin);
+      int8_t* base = Wq + (((key - key_base) * nch + ch) * KS * mb + gs * g * KS + bg) * (int64_t)kCore + core_off(rr, kin);
 #pragma unroll
       for (int i = 0; i < KS; ++i) base[(int64_t)i * mbg * kCore] = h ? di[i] : dr[i];
     }
@@ -304,6 +305,15 @@ struct I8Shape {
 };
 
 // dynamic smem: [NST W stages][NST B stages][src table fkeys*TT int32][keys fkeys int32][bars]
+//
+// Persistent grid: every CTA loops, claiming work items (tile, key chunk) in
+// increasing index order from an atomic counter.  The items of a tile are
+// chained in that order (item_seq): an item with seq > 0 waits for its tile's
+// ticket to reach seq before its epilogue.  The item it waits for has a lower
+// index, so it was claimed earlier by a CTA that is already running -- the
+// chain always progresses, whatever the dispatch order, co-residency or
+// concurrent kernels (no reliance on blockIdx scheduling, no timeout).
+// One pass handles MB consecutive 128-row M-blocks starting at blk0.
 template <int MB, int TT, int KS, int NST, int NGW, int G>
 __global__ void __maxnreg__(128)
     k_m2l_i8(const int32_t* __restrict__ item_tile, const int32_t* __restrict__ item_seq,
@@ -314,8 +324,8 @@ __global__ void __maxnreg__(128)
              const uint8_t* __restrict__ tile_cnt, const int8_t* __restrict__ Wq, const int8_t* __restrict__ Mq,
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
-             int* __restrict__ err, int item0, int nkq, int n_pad, int fkeys, int mb_tot, int grp, int tick_off,
-             int64_t key_base, int nrhs) {
+             int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int fkeys, int mb_tot,
+             int blk0, int tick_off, int64_t key_base, int nrhs) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int NT = S::THREADS;
@@ -329,16 +339,10 @@ __global__ void __maxnreg__(128)
   uint64_t* empty = fullb + NST;   // MMAs of the stage done (tcgen05.commit)
   uint64_t* done = empty + NST;    // all MMAs of the item done
   uint32_t* tbase_s = reinterpret_cast<uint32_t*>(done + 1);
+  __shared__ int s_item;
+  __shared__ double csc[TT];  // S_W S_V of each tile column (its rhs' moment scale)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int item = item0 + (int)blockIdx.x;
-  const int64_t k0 = item_k0[item], k1 = item_k1[item];
-  const int nk = (int)(k1 - k0);
   const int kp = 2 * nkq, nch = kp / kKC;
-  const int tile = item_tile[item];
-
-  // per-item metadata: uncompacted source slot of every (key, target column)
-  for (int i = tid; i < nk * TT; i += NT) srcf[i] = -1;
-  for (int i = tid; i < nk; i += NT) keys[i] = tile_keys[k0 + i];
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + s, 1);
@@ -352,92 +356,20 @@ __global__ void __maxnreg__(128)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  __syncthreads();
-  for (int i = tid; i < nk * TT; i += NT) {
-    const int64_t kk = k0 + i / TT;
-    const int j = i % TT;
-    if (j < tile_cnt[kk]) srcf[(i / TT) * TT + tile_cols[kk * TT + j]] = tile_src[kk * TT + j];
-  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tbase_s;
 
-  // warp roles: warp 0 lane 0 streams W (cp.async.bulk), warp 1 lane 0 issues
-  // the MMAs, warps 2-3 gather the moment digits (cp.async); NST stages in a ring
-  const int Q = nk * nch;
-  if (warp == 0) {
-    // the whole warp walks the ring (no divergent spinning lanes); lane 0 issues
-    int kq = 0, ch = 0;
-    for (int q = 0; q < Q; ++q) {
-      const int s = q % NST;
-      if (q >= NST) mbar_wait_sleep(empty + s, (uint32_t)((q / NST - 1) & 1));
-      if (lane == 0) {
-        if (FDH_I8_EXP & 2) {
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
-        } else {
-          mbar_expect_tx(full + s, S::WST);
-          bulk_g2s(wst + s * S::WST,
-                   Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (KS * mb_tot * kCore) + grp * (2 * KS * kCore),
-                   S::WST, full + s);
-        }
-      }
-      __syncwarp();
-      if (++ch == nch) {
-        ch = 0;
-        ++kq;
-      }
-    }
-  } else if (warp == 1) {
-    const uint64_t dA0 = sdesc(smem_u32(wst)), dB0 = sdesc(smem_u32(bst));
-    for (int q = 0; q < Q; ++q) {
-      const int s = q % NST;
-      const uint32_t ph = (uint32_t)((q / NST) & 1);
-      mbar_wait(full + s, ph);
-      mbar_wait(fullb + s, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        // descriptors are linear in the address (14-bit field, addr >> 4): every
-        // operand offset below is a compile-time constant added to the stage base
-        // (keeps the issuing thread at ~3 instructions per MMA; recomputing the
-        // descriptors per MMA made issue, not the tensor core, the bound)
-        const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-        const uint32_t acc0 = q > 0 ? 1u : 0u;
-#pragma unroll
-        for (int i = 0; i < KS; ++i) {
-          const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
-#pragma unroll
-          for (int b = 0; b < MB; ++b) {
-            // N > 256 splits into equal parts (multiples of 32 columns) with
-            // FDH_I8_BALANCED: e.g. 320 -> 160 + 160 rather than 256 + 64
-            const int nsp = (ncol + 255) / 256;
-            const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
-#pragma unroll
-            for (int p0 = 0; p0 < ncol;) {
-              const int np = ncol - p0 < part ? ncol - p0 : part;
-              mma_i8(tmem + b * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
-                     dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
-              p0 += np;
-            }
-          }
-        }
-        mma_commit(empty + s);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) mma_commit(done);
-    __syncwarp();
-  } else {
-    // gather: G groups of cp.async in flight per thread; a stage's arrival on
-    // fullb follows its own wait_group + proxy fence.  Work unit = (group of 4
-    // target columns, round of 8 pieces): lane = (column in the group, piece),
-    // so every warp instruction reads 4 contiguous 128-byte runs of Mq and
-    // writes 4 SMEM wavefronts.  Per-lane offsets are stage-invariant.
-    constexpr int RND = (KS * 4 + 7) / 8;  // rounds of 8 pieces per column (pieces: digit, kb, h)
-    constexpr int U = (TT / 4) * RND;
-    constexpr int UPW = (U + NGW - 1) / NGW;
+  // gather lane plan (stage-invariant): work unit = (group of 4 target columns,
+  // round of 8 pieces); lane = (column in the group, piece), so every warp
+  // instruction reads 4 contiguous 128-byte runs of Mq and writes 4 SMEM wavefronts
+  constexpr int RND = (KS * 4 + 7) / 8;  // rounds of 8 pieces per column (pieces: digit, kb, h)
+  constexpr int U = (TT / 4) * RND;
+  constexpr int UPW = (U + NGW - 1) / NGW;
+  int dsto[UPW], gofs[UPW], ccol[UPW];
+  if (warp >= 2) {
     const int cl = lane >> 3, p8 = lane & 7;
-    int dsto[UPW], gofs[UPW], ccol[UPW];
 #pragma unroll
     for (int t = 0; t < UPW; ++t) {
       const int u = (warp - 2) + t * NGW;
@@ -451,115 +383,202 @@ __global__ void __maxnreg__(128)
       gofs[t] = pc * 16;
       ccol[t] = ok ? c : 0;
     }
-    int kq = 0, ch = 0;
-    auto arrive = [&](int qa) {  // one arrival per warp once all its lanes' pieces landed
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
-    };
-    for (int q = 0; q < Q; ++q) {
-      const int s = q % NST;
-      if (q >= NST) mbar_wait_sleep(empty + s, (uint32_t)((q / NST - 1) & 1));
-      uint8_t* bb = bst + s * S::BST;
-      const int32_t* sf = srcf + kq * TT;
-      const int8_t* mq = Mq + (int64_t)ch * (KS * 64);
-#pragma unroll
-      for (int t = 0; t < UPW; ++t) {
-        if (dsto[t] < 0 || (FDH_I8_EXP & 1)) continue;
-        const int src = sf[ccol[t]];
-        if (src >= 0) cp_async16(bb + dsto[t], mq + (int64_t)src * nch * (KS * 64) + gofs[t]);
-        else *reinterpret_cast<int4*>(bb + dsto[t]) = make_int4(0, 0, 0, 0);
-      }
-      cp_async_commit();
-      if (q >= G) {
-        cp_async_wait<G>();
-        arrive(q - G);
-      }
-      if (++ch == nch) {
-        ch = 0;
-        ++kq;
-      }
-    }
-    cp_async_wait<0>();
-    for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qa);
   }
-  // all MMAs of the item done
-  mbar_wait_sleep(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  // ---- epilogue: levels -> FP64, chained accumulation into the tile
-  const int seq = item_seq[item], nit = tile_nitem[tile];
-  const int lvl = tile_level[tile];
-  const int exw = level_exp(lvmax_w, lvl) + 2;
-  __shared__ double csc[TT];  // S_W S_V of each tile column (its rhs' moment scale)
-  if (tid < TT) csc[tid] = ldexp(1.0, exw + level_exp(lvmax_v, (tid % nrhs) * kMaxLevels + lvl));
-  __syncthreads();
-  if (seq > 0) {
-    if (tid == 0) {
-      long long spins = 0;
-      while (ld_acquire(ticket + tick_off + tile) != seq) {
-        __nanosleep(200);
-        if (++spins > (1ll << 26)) {  // > ~10 s: report instead of hanging
-          atomicOr(err, 2);
-          break;
-        }
-      }
+  uint32_t qbase = 0;  // ring stages consumed by the previous items of this CTA
+#pragma unroll 1
+  for (int it = 0;; ++it) {
+    if (tid == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int idx = s_item;
+    if (idx >= n_item) break;
+    const int item = item0 + idx;
+    const int64_t k0 = item_k0[item], k1 = item_k1[item];
+    const int nk = (int)(k1 - k0);
+    const int tile = item_tile[item];
+    // per-item metadata: uncompacted source slot of every (key, target column)
+    for (int i = tid; i < nk * TT; i += NT) srcf[i] = -1;
+    for (int i = tid; i < nk; i += NT) keys[i] = tile_keys[k0 + i];
+    const int lvl = tile_level[tile];
+    const int exw = level_exp(lvmax_w, lvl) + 2;
+    if (tid < TT) csc[tid] = ldexp(1.0, exw + level_exp(lvmax_v, (tid % nrhs) * kMaxLevels + lvl));
+    __syncthreads();
+    for (int i = tid; i < nk * TT; i += NT) {
+      const int64_t kk = k0 + i / TT;
+      const int j = i % TT;
+      if (j < tile_cnt[kk]) srcf[(i / TT) * TT + tile_cols[kk * TT + j]] = tile_src[kk * TT + j];
     }
     __syncthreads();
-  }
-  const bool last = seq == nit - 1;
-  double fL[S::LV];  // level weights 2^(-7(L+2)); the power-of-two scale S_W S_V of the
-                    // column's rhs is applied after the (exact) level sum
-#pragma unroll
-  for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
-  double* A = tile_acc + (int64_t)tile * n_pad * NC;
-  const int qw = warp & 3;  // TMEM lane quarter of this warp
-#pragma unroll 1
-  for (int b = 0; b < MB && (NGW == 2 || (warp >= 2 && warp < 6)); ++b) {
-    const int row = (2 * grp + b) * 128 + qw * 32 + lane;
-#pragma unroll 1
-    for (int g = 0; g < NC / 8; ++g) {
-      uint32_t r[S::LV][8];
-#pragma unroll
-      for (int L = 0; L < S::LV; ++L)
-        tmem_ld8(tmem + ((uint32_t)(qw * 32) << 16) + b * S::LV * NC + L * NC + 8 * g, r[L]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row >= n_pad) continue;
-      double v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        double a = 0.0;
-#pragma unroll
-        for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
-        v[e] = a * csc[(8 * g + e) >> 1];  // exact: a power of two
+
+    // warp roles: warp 0 streams W (cp.async.bulk), warp 1 issues the MMAs,
+    // warps 2.. gather the moment digits (cp.async); NST stages in a ring whose
+    // position continues across items (stage qg = qbase + q)
+    const int Q = nk * nch;
+    if (warp == 0) {
+      // the whole warp walks the ring (no divergent spinning lanes); lane 0 issues
+      int kq = 0, ch = 0;
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
+        if (lane == 0) {
+          if (FDH_I8_EXP & 2) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
+          } else {
+            mbar_expect_tx(full + s, S::WST);
+            bulk_g2s(wst + s * S::WST,
+                     Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (KS * mb_tot * kCore) + blk0 * (KS * kCore),
+                     S::WST, full + s);
+          }
+        }
+        __syncwarp();
+        if (++ch == nch) {
+          ch = 0;
+          ++kq;
+        }
       }
-      double* pa = A + (int64_t)row * NC + 8 * g;
-      if (seq > 0) {
+    } else if (warp == 1) {
+      const uint64_t dA0 = sdesc(smem_u32(wst)), dB0 = sdesc(smem_u32(bst));
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        const uint32_t ph = (qg / NST) & 1;
+        mbar_wait(full + s, ph);
+        mbar_wait(fullb + s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          // descriptors are linear in the address (14-bit field, addr >> 4): every
+          // operand offset below is a compile-time constant added to the stage base
+          // (keeps the issuing thread at ~3 instructions per MMA)
+          const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
+          const uint32_t acc0 = q > 0 ? 1u : 0u;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] += __ldcg(pa + e);
+          for (int i = 0; i < KS; ++i) {
+            const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
+#pragma unroll
+            for (int b = 0; b < MB; ++b) {
+              // N > 256 splits into equal parts (multiples of 32 columns)
+              const int nsp = (ncol + 255) / 256;
+              const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
+#pragma unroll
+              for (int p0 = 0; p0 < ncol;) {
+                const int np = ncol - p0 < part ? ncol - p0 : part;
+                mma_i8(tmem + b * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
+                       dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
+                p0 += np;
+              }
+            }
+          }
+          mma_commit(empty + s);
+        }
+        __syncwarp();
       }
-      if (last) {
+      if (lane == 0) mma_commit(done);
+      __syncwarp();
+    } else {
+      // gather: G groups of cp.async in flight per thread; a stage's arrival on
+      // fullb follows its own wait_group + proxy fence
+      int kq = 0, ch = 0;
+      auto arrive = [&](uint32_t qa) {  // one arrival per warp once all its lanes' pieces landed
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
+      };
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
+        uint8_t* bb = bst + s * S::BST;
+        const int32_t* sf = srcf + kq * TT;
+        const int8_t* mq = Mq + (int64_t)ch * (KS * 64);
+#pragma unroll
+        for (int t = 0; t < UPW; ++t) {
+          if (dsto[t] < 0 || (FDH_I8_EXP & 1)) continue;
+          const int src = sf[ccol[t]];
+          if (src >= 0) cp_async16(bb + dsto[t], mq + (int64_t)src * nch * (KS * 64) + gofs[t]);
+          else *reinterpret_cast<int4*>(bb + dsto[t]) = make_int4(0, 0, 0, 0);
+        }
+        cp_async_commit();
+        if (q >= G) {
+          cp_async_wait<G>();
+          arrive(qg - G);
+        }
+        if (++ch == nch) {
+          ch = 0;
+          ++kq;
+        }
+      }
+      cp_async_wait<0>();
+      for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qbase + qa);
+    }
+    // all MMAs of the item done
+    mbar_wait_sleep(done, it & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // ---- epilogue: levels -> FP64, chained accumulation into the tile
+    const int seq = item_seq[item], nit = tile_nitem[tile];
+    if (seq > 0) {
+      if (tid == 0)
+        while (ld_acquire(ticket + tick_off + tile) != seq) __nanosleep(100);
+      __syncthreads();
+    }
+    const bool last = seq == nit - 1;
+    double fL[S::LV];  // level weights 2^(-7(L+2)); the power-of-two scale S_W S_V of the
+                       // column's rhs is applied after the (exact) level sum
+#pragma unroll
+    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
+    double* A = tile_acc + (int64_t)tile * n_pad * NC;
+    const int qw = warp & 3;  // TMEM lane quarter of this warp
+#pragma unroll 1
+    for (int b = 0; b < MB && (NGW == 2 || (warp >= 2 && warp < 6)); ++b) {
+      const int row = (blk0 + b) * 128 + qw * 32 + lane;
+#pragma unroll 1
+      for (int g = 0; g < NC / 8; ++g) {
+        uint32_t r[S::LV][8];
+#pragma unroll
+        for (int L = 0; L < S::LV; ++L)
+          tmem_ld8(tmem + ((uint32_t)(qw * 32) << 16) + b * S::LV * NC + L * NC + 8 * g, r[L]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row >= n_pad) continue;
+        double v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int col = 8 * g + e;
-          const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
-          if (ts >= 0) loc[(int64_t)ts * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
-        }
-      } else {
+          double a = 0.0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) __stcg(pa + e, v[e]);
+          for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
+          v[e] = a * csc[(8 * g + e) >> 1];  // exact: a power of two
+        }
+        double* pa = A + (int64_t)row * NC + 8 * g;
+        if (seq > 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] += __ldcg(pa + e);
+        }
+        if (last) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = 8 * g + e;
+            const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
+            if (ts >= 0) loc[(int64_t)ts * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) __stcg(pa + e, v[e]);
+        }
       }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    if (!last) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release(ticket + tick_off + tile, seq + 1);
+    } else {
+      __syncthreads();
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    qbase += (uint32_t)Q;
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  if (!last) {
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release(ticket + tick_off + tile, seq + 1);
-  }
 }
 
 template <int MB, int TT, int NST, int NGW>
@@ -569,22 +588,32 @@ size_t i8_smem(int fkeys) {
 }
 
 template <int MB, int TT, int NST, int NGW, int G>
-void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int grp) {
+void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass) {
   using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
   auto kern = k_m2l_i8<MB, TT, kI8Digits, NST, NGW, G>;
   const size_t sm = i8_smem<MB, TT, NST, NGW>(a.fkeys);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  kern<<<a.n_item, S::THREADS, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
-                                         a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
-                                         a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.err, a.item0, a.nkq,
-                                         a.n_pad, a.fkeys, mb_tot, grp, grp * a.n_tile, a.key_base, a.nrhs);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, sm);
+  const int grid = std::max(1, std::min(a.n_item, nsm * std::max(1, per_sm)));
+  kern<<<grid, S::THREADS, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem, a.tile_tslot,
+                                     a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
+                                     a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.counter + pass, a.item0,
+                                     a.n_item, a.nkq, a.n_pad, a.fkeys, mb_tot, blk0, pass * a.n_tile, a.key_base,
+                                     a.nrhs);
 }
 
 }  // namespace
 
 int m2l_i8_supported(int n, int tile) {
   const int mb = (n + 127) / 128;
-  return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && tile == 16);
+  return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && (tile == 16 || tile == 32));
 }
 int m2l_i8_fkeys(int nkq) {
   // |digit| <= 64: one key adds at most KS * KP * 64^2 to a level accumulator
@@ -597,11 +626,11 @@ int64_t m2l_i8_mbytes_per_slot(int nkq) { return (int64_t)kI8Digits * 2 * 2 * nk
 
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                         const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
-                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int64_t key_base) {
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int gs, int64_t key_base) {
   if (nkeys <= 0) return;
   dim3 grid((unsigned)nkeys, (unsigned)((n + kCplRows - 1) / kCplRows));
   k_coupling_i8<kI8Digits><<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
-                                                 (n + 127) / 128, key_base);
+                                                 (n + 127) / 128, gs, key_base);
 }
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
                       int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs) {
@@ -614,25 +643,31 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
   const int mb = (n + 127) / 128;
-  static const int var = [] {
-    const char* e = std::getenv("FDH_I8_VARIANT");  // tuning knob
-    return e ? std::atoi(e) : 0;
-  }();
-  // measured on config 2 (M2L ms): 2 gather warps 38.6, 4: 31.0, 8: 30.2 (G = 1 or 2: same)
+  // passes over the item list (m2l_i8_passes): one per M-block group; a.counter
+  // holds one zeroed claim counter per pass (and per on-the-fly segment)
   if (mb == 1 && tile == 32) {
-    if (var == 1) run_i8<1, 32, 4, 4, 1>(st, a, 1, 0);
-    else run_i8<1, 32, 4, 8, 1>(st, a, 1, 0);
+    run_i8<1, 32, 4, 8, 1>(st, a, 1, 0, 0);
   } else if (mb == 2 && tile == 16) {
-    if (var == 1) run_i8<2, 16, 3, 4, 1>(st, a, 2, 0);
-    else run_i8<2, 16, 3, 8, 1>(st, a, 2, 0);
+    run_i8<2, 16, 3, 8, 1>(st, a, 2, 0, 0);
   } else if (mb == 3 && tile == 16) {
     // 352 rows (m = 6): TMEM holds 7 levels x 32 columns for two M-blocks only, so
     // the rows run as two M-block groups {0, 1} and {2}, each its own pass over the
     // items with its own ticket chain (same moment gather, disjoint W and rows)
-    run_i8<2, 16, 3, 8, 1>(st, a, 3, 0);
-    run_i8<1, 16, 4, 8, 1>(st, a, 3, 1);
-  } else return 1;
+    run_i8<2, 16, 3, 8, 1>(st, a, 3, 0, 0);
+    run_i8<1, 16, 4, 8, 1>(st, a, 3, 2, 1);
+  } else if (mb >= 2 && tile == 32) {
+    // 32 target columns (N up to 448 per W digit): one 128-row M-block per pass
+    for (int b = 0; b < mb; ++b) run_i8<1, 32, 4, 8, 1>(st, a, mb, b, b);
+  } else {
+    return 1;
+  }
   return 0;
 }
+int m2l_i8_passes(int n, int tile) {
+  const int mb = (n + 127) / 128;
+  if (tile == 32) return mb;
+  return mb > 2 ? 2 : 1;
+}
+int m2l_i8_wgroup(int n, int tile) { return (tile == 16 && (n + 127) / 128 >= 2) ? 2 : 1; }
 
 }  // namespace fdhelm

@@ -52,6 +52,7 @@ struct M2LArgs {
   int* ticket = nullptr;
   double* loc = nullptr;
   int* err = nullptr;
+  int* counter = nullptr;  // zeroed item-claim counter (one per launch)
 };
 // returns 0 on success, nonzero if the n_pad / tile combination is not compiled
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a);
@@ -79,15 +80,18 @@ struct M2LI8Args {
   int64_t key_base = 0;  // first key of the Wq buffer (on-the-fly segments)
   int nrhs = 1;          // moment scales per (rhs, level): lvmax_v[rhs * kMaxLevels + level];
                          // tile column c = (slot, rhs) with rhs = c % nrhs
+  int* counter = nullptr;  // zeroed item-claim counters, one per M-block pass (persistent grid)
 };
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
 int64_t m2l_i8_wbytes_per_key(int n, int nkq);
 int64_t m2l_i8_mbytes_per_slot(int nkq);
+// gs: M-blocks per W group (m2l_i8_wgroup)
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
                         const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, int pass,
-                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int64_t key_base = 0);
-inline int m2l_i8_groups(int n) { return (n + 127) / 128 > 2 ? 2 : 1; }  // M-block groups per tile
+                        unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int gs, int64_t key_base = 0);
+int m2l_i8_passes(int n, int tile);  // M-block passes over the items (= ticket chains / claim counters)
+int m2l_i8_wgroup(int n, int tile);  // M-blocks stored together per W group (2: {0,1},{2}; 1: per block)
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
                       int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs = 1);
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a);

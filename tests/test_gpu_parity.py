@@ -283,3 +283,86 @@ def test_overlapped_near_field_same_bits(monkeypatch):
     y = F.DirectionalOperator(*args).apply(q)
     monkeypatch.setenv("FDH_OVERLAP_NEARFIELD", "1")
     assert np.array_equal(F.DirectionalOperator(*args).apply(q), y)
+
+
+@pytest.mark.parametrize("impl", ["i8", "dmma"])
+def test_m2l_progress_with_concurrent_kernel(impl, monkeypatch):
+    """The M2L item chains progress whatever the CTA dispatch order: a CTA claims
+    its item from an atomic counter only once it runs, so every item an epilogue
+    waits for is held by a running CTA.  A long GEMM on another stream competes
+    for the SMs; y is bitwise the same as alone."""
+    import torch
+
+    if impl == "dmma":
+        monkeypatch.setenv("FDH_M2L_IMPL", "dmma")
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=40000, ns=30000)
+    op = F.DirectionalOperator(tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
+    y_ref = op.apply(q)
+    x = torch.from_numpy(q.view(np.float64).copy()).cuda()
+    y = torch.empty(2 * 40000, dtype=torch.float64, device="cuda")
+    a = torch.randn(4096, 4096, device="cuda")
+    s2 = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s2):
+        for _ in range(30):
+            a = torch.tanh(a @ a)
+    op.apply_device(x.data_ptr(), y.data_ptr())
+    with torch.cuda.stream(s2):
+        for _ in range(30):
+            a = torch.tanh(a @ a)
+    torch.cuda.synchronize()
+    op.sync()
+    assert np.array_equal(y.cpu().numpy().view(np.complex128), y_ref)
+
+
+@pytest.mark.parametrize("m", [5, 6])
+def test_m2l_int8_tile32_mblock_passes(m, monkeypatch):
+    """FDH_I8_TILE=32 for n > 128 nodes per box: 32 target columns (N up to 448 per
+    W digit), one 128-row M-block per pass over the items (W digits stored per
+    block) -- against the default 16-column tiles and the oracle."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=15000, ns=12000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    y16 = F.DirectionalOperator(*args).apply(q)
+    monkeypatch.setenv("FDH_I8_TILE", "32")
+    op = F.DirectionalOperator(*args)
+    assert op.stats()["m2l_impl"] == 1
+    y32 = op.apply(q)
+    yo = oracle.Oracle(*args).apply(q)
+    assert oracle.rel_l2(y32, yo) <= TOL and oracle.rel_l2(y32, y16) <= 1e-13
+    monkeypatch.setenv("FDH_W_ONTHEFLY", "1")
+    monkeypatch.setenv("FDH_W_SLOT_MB", "64")
+    op2 = F.DirectionalOperator(*args)
+    assert op2.stats()["w_segments"] >= 2
+    assert np.array_equal(op2.apply(q), y32)
+
+
+def test_multi_gpu_group_operator(monkeypatch):
+    """fdh_create(n_gpus): the in-library multi-GPU operator (one shard per device,
+    NCCL broadcast of x / reduce of y).  On this one-GPU box: the group path with
+    n_gpus = 1 (FDH_GROUP=1: NCCL communicator of one device) equals the plain
+    operator bitwise, and n_gpus beyond the device count is refused."""
+    import torch
+
+    c = CONFIGS[5]
+    tg, sr, q = make_inputs(c, nt=40000, ns=20000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, 4, c.eta2, c.l_hf)
+    y = F.DirectionalOperator(*args).apply(q)
+    monkeypatch.setenv("FDH_GROUP", "1")
+    g = F.DirectionalOperator(*args, n_gpus=1)
+    assert np.array_equal(g.apply(q), y)
+    x = torch.from_numpy(q.view(np.float64).copy()).cuda()
+    yd = torch.empty(2 * 40000, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    g.apply_device(x.data_ptr(), yd.data_ptr())
+    g.sync()
+    assert np.array_equal(yd.cpu().numpy().view(np.complex128), y)
+    assert len(g.owned_leaves()) > 0 and g.stats()["n_c"] > 0
+    n = torch.cuda.device_count()
+    with pytest.raises(F.FdhError) as e:
+        F.DirectionalOperator(*args, n_gpus=n + 1)
+    assert e.value.code == F.ERR_UNSUPPORTED
+    if n >= 2:
+        g2 = F.DirectionalOperator(*args, n_gpus=2)
+        assert oracle.rel_l2(g2.apply(q), y) <= 1e-14
