@@ -52,7 +52,9 @@ def workload_desc(c):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML in-process
+    (pynvml; no subprocess, so the sampler does not perturb short steps), else the
+    nvidia-smi query of the profiling recipe."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -65,7 +67,26 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        import pynvml as N
+
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append([str(sm), str(mx), hex(r)] + ["Active" if r & b else "Not Active" for b in bits])
+            self._stop.wait(self.period)
+
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            self.samples = []
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -315,7 +336,7 @@ def run_ours(args, c, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    with ClockSampler(local_rank, period=0.2 if args.config <= 2 else 1.0) as clk:
+    with ClockSampler(local_rank, period=0.1 if args.config <= 2 else 0.5) as clk:
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()  # L2 flush between timed steps (outside the step events)

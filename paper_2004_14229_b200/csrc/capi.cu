@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the library is resolved at run time (dlopen), see nccl()
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges per setup stage and apply phase
 
 #include <chrono>
 #include <thread>
@@ -473,7 +474,14 @@ void setup_device(fdh_op* o) {
     throw PlanError{4, "interpolation degree m=" + std::to_string(P.prm.m) + " has no compiled M2L kernel"};
 }
 
+// NVTX range per phase of the apply (host side: the launches / capture of the phase)
+const char* const kPhaseName[FDH_NPHASES + 1] = {"fdh:h2d", "fdh:s2m", "fdh:m2m", "fdh:m2l", "fdh:l2l",
+                                                 "fdh:l2t", "fdh:p2p", "fdh:d2h", "fdh:end"};
 void rec(fdh_op* o, int ph, cudaStream_t st) {
+  if (ph <= FDH_NPHASES) {
+    if (ph > 0) nvtxRangePop();
+    if (ph < FDH_NPHASES) nvtxRangePushA(kPhaseName[ph]);
+  }
   if (!o->timing) return;
   if (o->capturing_timed)  // an event-record node of the graph being captured
     CK(cudaEventRecordWithFlags(o->gev[ph], st, cudaEventRecordExternal));
@@ -831,10 +839,14 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
       if (const char* fk = std::getenv("FDH_M2L_FKEYS"))  // testing knob: shorter items (more chaining)
         prm.m2l_fkeys = std::max(1, std::min(prm.m2l_fkeys, std::atoi(fk)));
     }
+    nvtxRangePushA("fdh:setup:plan");
     build_plan(o->P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi, prm);
+    nvtxRangePop();
     if (device) {
       try {
+        nvtxRangePushA("fdh:setup:device");
         setup_device(o);
+        nvtxRangePop();
       } catch (const PlanError& e) {
         if (e.code != -1) throw;
         // int8 moment digits do not fit: rebuild with the FP64 DMMA path

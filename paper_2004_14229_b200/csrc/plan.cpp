@@ -6,6 +6,7 @@
 #include "plan.hpp"
 #include "setup_gpu.hpp"
 
+#include <nvtx3/nvToolsExt.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -924,6 +925,7 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
   P.n_pad = (P.n + 31) / 32 * 32;
   P.n_k = (P.n + 7) / 8 * 8;
   const auto t1 = std::chrono::steady_clock::now();
+  nvtxRangePushA("fdh:setup:structure");
   if (prm.gpu_structure) {
     // trees, partition, key directions, D / D^ and slots on the device (k_setup.cu)
     gpu_build_structure(P, tx, ty, tz, nt, sx, sy, sz, ns, lo, hi);
@@ -944,6 +946,7 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
     build_dirsets(P, P.T, true);
     build_dirsets(P, P.S, false);
   }
+  nvtxRangePop();
   P.structure_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
   // direction vector tables
   const int maxl = std::max(P.T.depth, P.S.depth);
@@ -989,9 +992,13 @@ void build_plan(Plan& P, const double* tx, const double* ty, const double* tz, i
   auto ts = std::chrono::steady_clock::now();
   if (std::getenv("FDH_DEBUG_SETUP"))
     std::fprintf(stderr, "[setup] structure    %9.1f ms\n", P.structure_ms);
+  nvtxRangePushA("fdh:setup:worklists");
   build_worklists(P);
+  nvtxRangePop();
   tick("worklists", ts);
+  nvtxRangePushA("fdh:setup:m2l_tiles");
   build_m2l(P);
+  nvtxRangePop();
   tick("m2l tiles", ts);
   // statistics
   for (auto& B : P.blocks) {
