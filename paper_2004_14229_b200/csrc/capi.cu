@@ -371,7 +371,8 @@ void setup_device(fdh_op* o) {
   o->mom = o->alloc<double>((size_t)(R * P.S.nslots * np2));  // [rhs][slot][Re | Im]
   o->loc = o->alloc<double>((size_t)(R * P.T.nslots * np2));
   o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
-  o->ticket = o->alloc<int>((size_t)std::max(3 * o->n_tile, 1));  // int8: one chain per M-block pass (<= 3)
+  o->ticket = o->alloc<int>((size_t)std::max(
+      (P.prm.m2l_impl == 1 ? m2l_i8_passes(P.n, P.prm.tile) : 1) * o->n_tile, 1));  // one chain per M-block pass
   o->q = o->alloc<double2>((size_t)(R * o->ns));
   o->q4 = o->alloc<double2>((size_t)(R * o->ns));
   {
@@ -470,8 +471,8 @@ void setup_device(fdh_op* o) {
   o->counter = o->alloc<int>(std::max<size_t>(1, o->segs.size()));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(o->st));
-  if (o->n_item > 0 && P.prm.m > 6)
-    throw PlanError{4, "interpolation degree m=" + std::to_string(P.prm.m) + " has no compiled M2L kernel"};
+  if (o->n_item > 0 && P.prm.m > 6)  // the FP64 DMMA kernels are compiled for m <= 6 (int8 path: any m)
+    throw PlanError{4, "interpolation degree m=" + std::to_string(P.prm.m) + " has no compiled FP64 M2L kernel"};
 }
 
 // NVTX range per phase of the apply (host side: the launches / capture of the phase)
@@ -828,13 +829,16 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
     const int nbox = (m + 1) * (m + 1) * (m + 1);
     const char* mi = std::getenv("FDH_M2L_IMPL");
     const char* pi = std::getenv("FDH_PLAN_I8");  // analysis knob: plan-only operators with the int8 plan
-    const bool want_i8 = (device || (pi && pi[0] == '1')) && m >= 1 && nbox <= 384 &&
-                         !(mi && std::string(mi) == "dmma");
+    const bool want_i8 = (device || (pi && pi[0] == '1')) && m >= 1 && !(mi && std::string(mi) == "dmma");
     if (want_i8) {
       prm.m2l_impl = 1;
-      prm.tile = nbox <= 128 ? 32 : 16;
-      if (const char* tt = std::getenv("FDH_I8_TILE"))  // 32: one M-block per pass for m = 5, 6 (N up to 448)
-        prm.tile = std::atoi(tt) == 32 ? 32 : prm.tile;
+      // 16 target columns for two / three M-blocks (m = 5, 6); beyond, one 128-row
+      // M-block per pass with 32 columns (any degree: m = 7 .. 10)
+      // 32 target columns for one M-block (m <= 4) and beyond three (m >= 7); for
+      // m = 5, 6 the planner chooses 16 or 32 from the sampled key-list overlap
+      prm.tile = (nbox <= 128 || nbox > 384) ? 32 : -1;
+      if (const char* tt = std::getenv("FDH_I8_TILE"))  // testing knob: force 16 or 32 for m = 5, 6
+        prm.tile = prm.tile > 0 ? prm.tile : (std::atoi(tt) == 32 ? 32 : 16);
       prm.m2l_fkeys = m2l_i8_fkeys((nbox + 15) / 16 * 16);
       if (const char* fk = std::getenv("FDH_M2L_FKEYS"))  // testing knob: shorter items (more chaining)
         prm.m2l_fkeys = std::max(1, std::min(prm.m2l_fkeys, std::atoi(fk)));

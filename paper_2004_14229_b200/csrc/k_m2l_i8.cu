@@ -613,7 +613,7 @@ void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass)
 
 int m2l_i8_supported(int n, int tile) {
   const int mb = (n + 127) / 128;
-  return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && (tile == 16 || tile == 32));
+  return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && tile == 16) || (mb >= 2 && tile == 32);
 }
 int m2l_i8_fkeys(int nkq) {
   // |digit| <= 64: one key adds at most KS * KP * 64^2 to a level accumulator

@@ -488,12 +488,13 @@ void build_m2l(Plan& P) {
   } while (0)
   const TreePlan& T = P.T;
   const TreePlan& S = P.S;
-  const int TT = P.prm.tile;
+  int TT = P.prm.tile;  // < 0: choose 16 or 32 target columns below (int8 M2L, 2-3 M-blocks)
   // multiple right-hand sides: a tile holds TT / R target slots x R rhs; the
   // column of (slot i of the tile, rhs r) is i * R + r and refers to the
   // rhs-major slot id r * nslots + slot (moments / locals stored per rhs)
   const int R = P.prm.nrhs;
-  if (R < 1 || R > TT || TT % R != 0) throw PlanError{1, "nrhs must divide the M2L tile width " + std::to_string(TT)};
+  if (R < 1 || R > std::abs(TT) || std::abs(TT) % R != 0)
+    throw PlanError{1, "nrhs must divide the M2L tile width " + std::to_string(std::abs(TT))};
   // pairs (target slot, key, source slot) grouped by target slot: parallel
   // counting pass, prefix, parallel scatter with atomic cursors (the order
   // inside a slot is then fixed by the per-slot sort by key -- keys are unique
@@ -559,6 +560,50 @@ void build_m2l(Plan& P) {
     return ((int64_t)l << 40) | ((int64_t)T.slot_dir[t] << 8) | par;
   };
   std::stable_sort(ts.begin(), ts.end(), [&](int32_t a, int32_t b) { return gkey(a) < gkey(b); });
+  std::vector<int32_t> key_lo(64, 0), key_hi(64, 0);
+  for (int32_t k = (int32_t)P.key_level.size() - 1; k >= 0; --k) key_lo[P.key_level[k]] = k;
+  for (int32_t k = 0; k < (int32_t)P.key_level.size(); ++k) key_hi[P.key_level[k]] = k + 1;
+  if (TT < 0) {
+    // int8 M2L with 2-3 M-blocks: 16 target columns (one pass over M-blocks {0,1}
+    // [+ {2}]) or 32 (one pass per M-block: twice the columns per W byte, the
+    // issued rate measured 1.14-1.18x higher, profiles/r02_m2l_sweep_tt_chunk.jsonl)
+    // -- but the union of a wider tile's key lists leaves more columns absent
+    // (clustered sources: config 5).  Estimated on every 8th 32-wide tile: the
+    // tile-keys of it and of its two 16-wide halves; 32 when 32 K32 / 1.16 < 16 K16.
+    const int64_t w32 = 32 / R, w16 = 16 / R;
+    std::vector<std::pair<int64_t, int64_t>> smp;  // [begin, end) into ts of sampled 32-wide tiles
+    for (size_t i = 0; i < ts.size();) {
+      size_t j = i;
+      const int64_t g = gkey(ts[i]);
+      while (j < ts.size() && gkey(ts[j]) == g) ++j;
+      int64_t q = 0;
+      for (size_t k = i; k < j; k += w32, ++q)
+        if ((q & 7) == 0) smp.push_back({(int64_t)k, (int64_t)std::min(j, k + w32)});
+      i = j;
+    }
+    int64_t k16 = 0, k32 = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : k16, k32)
+    for (int64_t si = 0; si < (int64_t)smp.size(); ++si) {
+      const int64_t b = smp[si].first, e = smp[si].second;
+      const int l = T.slot_level[ts[b]];
+      const int32_t kb = key_lo[l], kr = key_hi[l] - kb;
+      thread_local std::vector<uint8_t> mk;
+      mk.assign(kr, 0);
+      for (int64_t i = b; i < e; ++i) {
+        const uint8_t bit = (i - b) < w16 ? 1 : 2;
+        for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) mk[sk[q] - kb] |= bit;
+      }
+      for (int32_t k = 0; k < kr; ++k) {
+        k32 += mk[k] != 0;
+        k16 += (mk[k] & 1) + (mk[k] >> 1);
+      }
+    }
+    TT = (32.0 * (double)k32 / 1.16 < 16.0 * (double)k16) ? 32 : 16;
+    P.prm.tile = TT;
+    if (mdbg)
+      std::fprintf(stderr, "[m2l] tile width: sampled tile-keys 16: %lld, 32: %lld -> %d\n", (long long)k16,
+                   (long long)k32, TT);
+  }
   std::vector<int64_t> tile_first;  // index into ts
   for (size_t i = 0; i < ts.size();) {
     size_t j = i;
@@ -570,9 +615,6 @@ void build_m2l(Plan& P) {
   tile_first.push_back((int64_t)ts.size());
   const int64_t ntile = (int64_t)tile_first.size() - 1;
   // a tile never spans two groups: clip at group boundaries
-  std::vector<int32_t> key_lo(64, 0), key_hi(64, 0);
-  for (int32_t k = (int32_t)P.key_level.size() - 1; k >= 0; --k) key_lo[P.key_level[k]] = k;
-  for (int32_t k = 0; k < (int32_t)P.key_level.size(); ++k) key_hi[P.key_level[k]] = k + 1;
   P.tile_level.assign(ntile, 0);
   P.tile_dir.assign(ntile, 0);
   P.tile_tslot.assign(ntile * TT, -1);
@@ -691,7 +733,9 @@ void build_m2l(Plan& P) {
   const int nkq = (P.n + 15) / 16 * 16;
   const int64_t wbytes = P.prm.m2l_impl == 1 ? (int64_t)7 * ((P.n + 127) / 128) * 128 * 2 * nkq
                                               : (int64_t)P.n_pad * m2l_wplanes(P.n_pad) * P.n_k * 8;
-  int64_t chunk_mb = P.prm.m2l_impl == 1 ? 24 : 12;  // DMMA: optimum 8-12 MB (profiles/r01_m2l_chunk_sweep.txt)
+  // int8: 48 MB (profiles/r02_m2l_sweep_tt_chunk.jsonl: 2-3 % faster than 24 MB on configs 3, 5
+  // and the m = 6 shape); DMMA: optimum 8-12 MB (profiles/r01_m2l_chunk_sweep.txt)
+  int64_t chunk_mb = P.prm.m2l_impl == 1 ? 48 : 12;
   if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
   const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
   P.m2l_chunk = cw;

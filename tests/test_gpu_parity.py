@@ -318,12 +318,14 @@ def test_m2l_progress_with_concurrent_kernel(impl, monkeypatch):
 
 @pytest.mark.parametrize("m", [5, 6])
 def test_m2l_int8_tile32_mblock_passes(m, monkeypatch):
-    """FDH_I8_TILE=32 for n > 128 nodes per box: 32 target columns (N up to 448 per
-    W digit), one 128-row M-block per pass over the items (W digits stored per
-    block) -- against the default 16-column tiles and the oracle."""
+    """m = 5, 6 (2-3 M-blocks): 32 target columns (N up to 448 per W digit, one
+    128-row M-block per pass, W digits stored per block) against 16 columns (one
+    pass over M-blocks {0, 1} [+ {2}]) and the oracle; the planner picks one of
+    the two per operator (FDH_I8_TILE forces it)."""
     c = CONFIGS[2]
     tg, sr, q = make_inputs(c, nt=15000, ns=12000)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    monkeypatch.setenv("FDH_I8_TILE", "16")
     y16 = F.DirectionalOperator(*args).apply(q)
     monkeypatch.setenv("FDH_I8_TILE", "32")
     op = F.DirectionalOperator(*args)
@@ -366,3 +368,20 @@ def test_multi_gpu_group_operator(monkeypatch):
     if n >= 2:
         g2 = F.DirectionalOperator(*args, n_gpus=2)
         assert oracle.rel_l2(g2.apply(q), y) <= 1e-14
+
+
+@pytest.mark.parametrize("m", [7, 8])
+def test_high_degrees(m):
+    """Interpolation degree m >= 7 (the reference builders accept any m >= 0,
+    interpolation.cpp:9-20): the int8 M2L with one 128-row M-block per pass and
+    32 target columns (n = 512 / 729 nodes per box) against the oracle."""
+    rng = np.random.default_rng(200 + m)
+    tg = [rng.random(4000) for _ in range(3)]
+    sr = [rng.random(3500) for _ in range(3)]
+    q = rng.uniform(-1, 1, 3500) + 1j * rng.uniform(-1, 1, 3500)
+    y, yo, op, _ = run_pair(tg, sr, q, (0, 0, 0), (1, 1, 1), 12.0, 32, m, 1.0, -2)
+    st = op.stats()
+    assert st["m2l_impl"] == 1 and st["n_c"] > 0
+    err = oracle.rel_l2(y, yo)
+    print(f"m={m}: rel l2 vs oracle {err:.2e}")
+    assert err <= TOL
