@@ -94,6 +94,10 @@ typedef struct fdh_stats {
   double apply_ms_sum;          /* sum of apply_ms over the applies collected since the
                                    last fdh_set_timing (host-path applies: every one)      */
   int64_t applies_collected;
+  double aca_eps;               /* ACA tolerance in use (0: exact dense coupling)          */
+  double aca_mean_rank;         /* mean ACA rank over the compressed keys                  */
+  int64_t aca_bytes;            /* device bytes of the ACA factors                         */
+  int64_t aca_dense_keys;       /* keys kept dense (2 k n >= n^2)                          */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table
@@ -152,6 +156,14 @@ int fdh_apply_multi(fdh_op* op, const double* x, int64_t k, double* y);
  * kernel -> FDH_ERR_DOMAIN, as the reference's domain_error) are DEFERRED: they
  * accumulate over device-path applies and are returned by fdh_sync. */
 int fdh_apply_device(fdh_op* op, const double* x_dev, double* y_dev, void* stream);
+/* ACA-compressed coupling (opt-in and
+ * LOSSY): eps > 0 factorises every coupling matrix by partially pivoted ACA on
+ * the device (A ~ U V^*, pivoting as SPEC.md:457; a key whose rank would reach
+ * n/2 stays dense) and later applies run the M2L on the factors in FP64; results
+ * then agree with the exact apply to ~100 eps (eps = 1e-8 -> 1e-6),
+ * not to 1e-12.  eps = 0 returns to the exact M2L.  n <= 384 (m <= 6), nrhs = 1;
+ * FDH_ERR_MEMORY when the factors do not fit in device memory. */
+int fdh_set_aca(fdh_op* op, double eps);
 /* Wait for the operator's applies and return (and clear) the deferred device
  * error of the fdh_apply_device calls since the last fdh_sync. */
 int fdh_sync(fdh_op* op);

@@ -60,6 +60,10 @@ def lib():
         L.orc_leaf_points.restype = C.c_int64
         L.orc_stats.argtypes = [C.c_void_p, _i64]
         L.orc_last_timing.argtypes = [C.c_void_p, _d]
+        L.orc_set_aca.argtypes = [C.c_void_p, C.c_double]
+        L.orc_aca_ranks.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
+        L.orc_aca_ranks.restype = C.c_int64
+        L.orc_aca_compress.argtypes = [_d, C.c_int, C.c_double, C.c_int, _d, _d]
         for f in ("orc_export_tree", "orc_export_perm", "orc_export_dirsets"):
             getattr(L, f).argtypes = [C.c_void_p, C.c_int, _i64]
             getattr(L, f).restype = C.c_int64
@@ -184,6 +188,16 @@ class Oracle:
                                      y.view(np.float64).ctypes.data_as(_d)))
         rows = np.concatenate([self.leaf_points(0, int(i)) for i in lv]) if len(lv) else np.zeros(0, np.int64)
         return rows, y[rows]
+
+    def set_aca(self, eps):
+        """ACA-compressed coupling with tolerance eps (0 = dense)."""
+        _chk(lib().orc_set_aca(self.h, float(eps)))
+
+    def aca_ranks(self):
+        n = lib().orc_aca_ranks(self.h, None)
+        out = np.zeros(n, dtype=np.int32)
+        lib().orc_aca_ranks(self.h, out.ctypes.data_as(C.POINTER(C.c_int32)))
+        return out
 
     def last_timing(self):
         """Seconds of the last apply: upward, coupling generation, M2L products,
@@ -319,6 +333,20 @@ def export_digest(o):
     out.append(rows_digest(o.lminus()))
     out += [rows_digest(o.dirsets(0)), rows_digest(o.dirsets(1))]
     return out
+
+
+def aca_compress(A, eps, max_rank=None):
+    """SPEC.md aca_compress on one complex matrix: returns (U, W) with A ~ U @ W,
+    or None when the matrix stays dense (2 k n >= n^2)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    n = A.shape[0]
+    U = np.zeros(n * n, dtype=np.complex128)
+    W = np.zeros(n * n, dtype=np.complex128)
+    k = lib().orc_aca_compress(A.view(np.float64).ctypes.data_as(_d), n, float(eps), int(max_rank or n),
+                               U.view(np.float64).ctypes.data_as(_d), W.view(np.float64).ctypes.data_as(_d))
+    if k == 0:
+        return None
+    return U[:n * k].reshape(k, n).T.copy(), W[:n * k].reshape(k, n).copy()
 
 
 def rel_l2(a, b):

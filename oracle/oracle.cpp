@@ -378,6 +378,11 @@ struct Op {
   std::vector<std::tuple<int, int64_t, int64_t, int64_t>> keys;
   std::vector<int32_t> key_dir;
   std::vector<cplx> coupling;  // keys x n x n
+  // ACA-compressed coupling: per key rank k (0 = kept dense),
+  // U (n x k, column-major) and W = V^* (k x n, row-major); A ~ U W
+  double aca_eps = 0.0;
+  std::vector<int32_t> aca_rank;
+  std::vector<std::vector<cplx>> aca_u, aca_w;
   std::vector<double> Eref;    // 8 x n x n
   // per-box direction sets: dirs[node] sorted union; kind bitmask 1=D 2=D^
   std::vector<std::vector<int32_t>> dT, dS;
@@ -580,6 +585,94 @@ void build_coupling(Op& op) {
   }
 }
 
+// SPEC.md:440-448 aca_compress, with the pinned design decisions:
+// partially pivoted ACA on the n x n row-major matrix A: start from row 0; the
+// column pivot is the max-modulus entry of the residual row (lowest index on
+// ties), the next row pivot the max-modulus entry of the residual column among
+// the rows not used yet; stop when |u_k| |w_k| <= eps |S_k|_F with the standard
+// incremental Frobenius estimate of the accumulated approximation S_k, or at
+// max_rank.  Returns the rank k and A ~ U W (U n x k column-major, W = V^* k x n
+// row-major), or 0 (keep dense) when 2 k n >= n^2 (no gain).  A zero residual row
+// (exact low rank) ends the iteration.
+int aca_compress(const cplx* A, int n, double eps, int max_rank, std::vector<cplx>& U, std::vector<cplx>& W) {
+  U.clear();
+  W.clear();
+  std::vector<char> used(n, 0);
+  std::vector<cplx> row(n), col(n);
+  double s2 = 0.0;  // |S_k|_F^2 estimate
+  int ip = 0, k = 0;
+  const int kmax = std::min(max_rank, n);
+  while (k < kmax) {
+    used[ip] = 1;
+    for (int c = 0; c < n; ++c) {  // residual row ip
+      cplx v = A[(size_t)ip * n + c];
+      for (int q = 0; q < k; ++q) v -= U[(size_t)q * n + ip] * W[(size_t)q * n + c];
+      row[c] = v;
+    }
+    int jp = 0;
+    double best = -1.0;
+    for (int c = 0; c < n; ++c)
+      if (std::abs(row[c]) > best) {
+        best = std::abs(row[c]);
+        jp = c;
+      }
+    if (best == 0.0) break;  // residual row vanishes: exact rank k
+    const cplx delta = row[jp];
+    for (int i = 0; i < n; ++i) {  // residual column jp
+      cplx v = A[(size_t)i * n + jp];
+      for (int q = 0; q < k; ++q) v -= U[(size_t)q * n + i] * W[(size_t)q * n + jp];
+      col[i] = v;
+    }
+    // new cross u w with u = residual column, w = residual row / pivot
+    double nu = 0.0, nw = 0.0;
+    for (int i = 0; i < n; ++i) nu += std::norm(col[i]);
+    std::vector<cplx> w(n);
+    for (int c = 0; c < n; ++c) {
+      w[c] = row[c] / delta;
+      nw += std::norm(w[c]);
+    }
+    double cross = 0.0;  // 2 Re sum_q <u_q w_q, u w>_F = 2 Re sum_q (u_q^H u)(w_q^H w)
+    for (int q = 0; q < k; ++q) {
+      cplx a(0, 0), b(0, 0);
+      for (int i = 0; i < n; ++i) a += std::conj(U[(size_t)q * n + i]) * col[i];
+      for (int c = 0; c < n; ++c) b += std::conj(W[(size_t)q * n + c]) * w[c];
+      cross += 2.0 * (a * b).real();
+    }
+    if (k > 0 && std::sqrt(nu * nw) <= 1e-14 * std::sqrt(std::max(s2, 0.0))) break;  // round-off cross: exact rank k
+    U.insert(U.end(), col.begin(), col.end());
+    W.insert(W.end(), w.begin(), w.end());
+    ++k;
+    s2 += cross + nu * nw;
+    if (std::sqrt(nu * nw) <= eps * std::sqrt(std::max(s2, 0.0))) break;
+    int inext = -1;
+    best = -1.0;
+    for (int i = 0; i < n; ++i)
+      if (!used[i] && std::abs(col[i]) > best) {
+        best = std::abs(col[i]);
+        inext = i;
+      }
+    if (inext < 0) break;
+    ip = inext;
+  }
+  if (2 * (int64_t)k * n >= (int64_t)n * n) {  // no gain: keep dense
+    U.clear();
+    W.clear();
+    return 0;
+  }
+  return k;
+}
+
+void build_aca(Op& op) {
+  const int n = op.n;
+  const size_t nk = op.keys.size();
+  op.aca_rank.assign(nk, 0);
+  op.aca_u.assign(nk, {});
+  op.aca_w.assign(nk, {});
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t k = 0; k < (int64_t)nk; ++k)
+    op.aca_rank[k] = aca_compress(&op.coupling[(size_t)k * n * n], n, op.aca_eps, n, op.aca_u[k], op.aca_w[k]);
+}
+
 int32_t find_dir(const std::vector<int32_t>& d, int32_t c) {
   auto it = std::lower_bound(d.begin(), d.end(), c);
   if (it == d.end() || *it != c) return -1;
@@ -764,6 +857,23 @@ void apply(Op& op, const double* xin, double* yout, const std::vector<char>* lea
         A = Abuf.data();
       } else {
         A = &op.coupling[(size_t)bk.key * n * n];
+      }
+      if (op.aca_eps > 0.0 && op.aca_rank[bk.key] > 0) {  // A ~ U W: out += U (W in)
+        const int rk = op.aca_rank[bk.key];
+        const cplx* Uk = op.aca_u[bk.key].data();
+        const cplx* Wk = op.aca_w[bk.key].data();
+        cplx z[512];
+        for (int q = 0; q < rk; ++q) {
+          cplx acc(0, 0);
+          for (int k = 0; k < n; ++k) acc += Wk[(size_t)q * n + k] * in[k];
+          z[q] = acc;
+        }
+        for (int j = 0; j < n; ++j) {
+          cplx acc(0, 0);
+          for (int q = 0; q < rk; ++q) acc += Uk[(size_t)q * n + j] * z[q];
+          out[j] += acc;
+        }
+        continue;
       }
       for (int j = 0; j < n; ++j) {
         cplx acc(0, 0);
@@ -1215,6 +1325,27 @@ int orc_apply_sampled(orc_op* o, const double* x, const int64_t* leaf_idx, int64
     }
     apply(o->op, x, y, &mask);
   });
+}
+int orc_set_aca(orc_op* o, double eps) {
+  return guard([&] {
+    if (!(eps >= 0.0 && eps < 1.0)) throw Err(E_ARG, "ACA tolerance must be in [0, 1)");
+    if (eps > 0.0 && !o->op.with_coupling) throw Err(E_ARG, "ACA needs the stored coupling matrices (orc_create)");
+    o->op.aca_eps = eps;
+    if (eps > 0.0) build_aca(o->op);
+  });
+}
+int64_t orc_aca_ranks(const orc_op* o, int32_t* out) {
+  const int64_t nk = (int64_t)o->op.aca_rank.size();
+  if (out)
+    for (int64_t k = 0; k < nk; ++k) out[k] = o->op.aca_rank[k];
+  return nk;
+}
+int orc_aca_compress(const double* A, int n, double eps, int max_rank, double* U, double* W) {
+  std::vector<cplx> u, w;
+  const int k = aca_compress(reinterpret_cast<const cplx*>(A), n, eps, max_rank, u, w);
+  if (U) std::memcpy(U, u.data(), sizeof(cplx) * u.size());
+  if (W) std::memcpy(W, w.data(), sizeof(cplx) * w.size());
+  return k;
 }
 int orc_last_timing(const orc_op* o, double* out5) {
   for (int i = 0; i < 5; ++i) out5[i] = o->op.tim[i];

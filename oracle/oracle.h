@@ -96,6 +96,15 @@ int64_t orc_leaf_count(const orc_op* op, int which);
 int64_t orc_leaf_points(const orc_op* op, int which, int64_t leaf, int64_t* idx, int64_t cap);
 
 int orc_stats(const orc_op* op, int64_t* out /* ORC_NSTATS */);
+/* ACA-compressed coupling: eps > 0 compresses every stored
+ * coupling matrix by partially pivoted ACA (A ~ U V^*; dense kept where 2 k n >=
+ * n^2) and the M2L applies the factors; eps = 0 restores the dense M2L. */
+int orc_set_aca(orc_op* op, double eps);
+/* per-key ACA rank (0 = dense); returns the key count */
+int64_t orc_aca_ranks(const orc_op* op, int32_t* out);
+/* aca_compress on one n x n complex row-major matrix: returns k (0 = dense) and
+ * U (n x k complex, column-major), W = V^* (k x n complex, row-major) */
+int orc_aca_compress(const double* A, int n, double eps, int max_rank, double* U, double* W);
 /* Wall seconds of the last apply: [0] upward pass (S2M + M2M), [1] coupling
  * matrix generation (sampled-structure mode: once per key used), [2] M2L
  * products, [3] L2L + L2T + near field; [4] = coupling matrices generated. */

@@ -166,6 +166,15 @@ struct fdh_op {
   const void* gy = nullptr;
   cudaStream_t gst = nullptr;
   int64_t graph_replays = 0;
+  // ACA-compressed coupling (fdh_set_aca; opt-in, lossy): per-key rank (-1 dense),
+  // factor offsets and the factors, resident in HBM
+  double aca_eps = 0.0;
+  int32_t* aca_rank = nullptr;
+  int64_t *aca_uoff = nullptr, *aca_woff = nullptr;
+  double2 *aca_U = nullptr, *aca_W = nullptr;
+  std::vector<void*> aca_allocs;
+  int64_t aca_bytes = 0;
+  double aca_mean_rank = 0.0;
   // multi-GPU operator (fdh_create with n_gpus > 1): one target-leaf shard per
   // device (rank g of n_gpus on device g), y reduced to device 0 over NCCL
   std::vector<fdh_op*> parts;
@@ -182,6 +191,7 @@ struct fdh_op {
     if (st) cudaStreamSynchronize(st);
     if (gexec) cudaGraphExecDestroy(gexec);
     for (void* p : allocs) cudaFree(p);
+    for (void* p : aca_allocs) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_all)
@@ -537,7 +547,37 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     CK(cudaEventRecord(o->ev_nf, o->st2));
   }
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(R * lstr), st));
-  if (o->n_item > 0 && o->i8) {
+  if (o->n_item > 0 && o->aca_eps > 0.0) {
+    // ACA-compressed coupling (fdh_set_aca): the low-rank M2L over the same plan
+    CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
+    CK(cudaMemsetAsync(o->counter, 0, sizeof(int), st));
+    M2LAcaArgs a;
+    a.n_item = o->n_item;
+    a.item_tile = o->item_tile;
+    a.item_seq = o->item_seq;
+    a.item_k0 = o->item_k0;
+    a.item_k1 = o->item_k1;
+    a.tile_nitem = o->tile_nitem;
+    a.tile_tslot = o->tile_tslot;
+    a.tile_keys = o->tile_keys;
+    a.tile_src = o->tile_src;
+    a.tile_cols = o->tile_cols;
+    a.tile_cnt = o->tile_cnt;
+    a.rank = o->aca_rank;
+    a.uoff = o->aca_uoff;
+    a.woff = o->aca_woff;
+    a.U = o->aca_U;
+    a.W = o->aca_W;
+    a.mom = o->mom;
+    a.tile_acc = o->tile_acc;
+    a.ticket = o->ticket;
+    a.loc = o->loc;
+    a.counter = o->counter;
+    rec(o, FDH_NPHASES + 1, st);
+    if (launch_m2l_aca(st, n, np, P.prm.tile, a) != 0) throw PlanError{4, "ACA M2L: n > 384 not compiled"};
+    rec(o, FDH_NPHASES + 2, st);
+    L += 1;
+  } else if (o->n_item > 0 && o->i8) {
     const int npass = m2l_i8_passes(n, P.prm.tile);
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(npass * o->n_tile), st));
     CK(cudaMemsetAsync(o->counter, 0, sizeof(int) * (size_t)(npass * std::max<size_t>(1, o->segs.size())), st));
@@ -1084,6 +1124,94 @@ int fdh_apply_device(fdh_op* o, const double* x_dev, double* y_dev, void* stream
   });
 }
 
+int fdh_set_aca(fdh_op* o, double eps) {
+  if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  if (!(eps >= 0.0 && eps < 1.0)) return fail(FDH_ERR_ARG, "ACA tolerance must be in [0, 1)");
+  for (fdh_op* p : o->parts) {
+    cudaSetDevice(p->device);
+    if (const int rc = fdh_set_aca(p, eps)) return rc;
+  }
+  if (!o->parts.empty()) {
+    cudaSetDevice(0);
+    o->aca_eps = eps;
+    return FDH_OK;
+  }
+  if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
+  if (o->R != 1) return fail(FDH_ERR_UNSUPPORTED, "ACA with several right-hand sides is not supported");
+  return guard([&] {
+    CK(cudaSetDevice(o->device));
+    CK(cudaStreamSynchronize(o->st));
+    for (void* p : o->aca_allocs) cudaFree(p);
+    o->aca_allocs.clear();
+    o->aca_eps = 0.0;
+    o->aca_bytes = 0;
+    o->gx = nullptr;  // re-capture the apply graph
+    if (o->gexec) {
+      CK(cudaGraphExecDestroy(o->gexec));
+      o->gexec = nullptr;
+    }
+    if (eps == 0.0) return;
+    Plan& P = o->P;
+    const int n = P.n;
+    if (n > 384) throw PlanError{FDH_ERR_UNSUPPORTED, "ACA M2L is compiled for n <= 384 (m <= 6)"};
+    const int64_t nkeys = (int64_t)P.key_level.size();
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      const cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+      if (e != cudaSuccess) throw PlanError{FDH_ERR_MEMORY, "ACA factors do not fit in device memory"};
+      o->aca_allocs.push_back(p);
+      return p;
+    };
+    o->aca_rank = static_cast<int32_t*>(dalloc(sizeof(int32_t) * (size_t)nkeys));
+    // pass 0: ranks, in chunks of keys with a scratch of n (n + 1) complex per key
+    const int64_t chunk = 1024;
+    double2* scratch = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)(chunk * n * (n + 1))));
+    for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+      launch_aca_factor(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
+                        eps, n, 0, o->aca_rank, scratch, nullptr, nullptr, nullptr, nullptr);
+    CK(cudaGetLastError());
+    std::vector<int32_t> rk(nkeys);
+    CK(cudaMemcpyAsync(rk.data(), o->aca_rank, sizeof(int32_t) * nkeys, cudaMemcpyDeviceToHost, o->st));
+    CK(cudaStreamSynchronize(o->st));
+    cudaFree(scratch);
+    o->aca_allocs.pop_back();
+    std::vector<int64_t> uo(nkeys, 0), wo(nkeys, 0);
+    int64_t ut = 0, wt = 0, rsum = 0, nd = 0;
+    for (int64_t k = 0; k < nkeys; ++k) {
+      uo[k] = ut;
+      wo[k] = wt;
+      if (rk[k] < 0) {
+        wt += (int64_t)n * n;
+        ++nd;
+      } else {
+        ut += (int64_t)rk[k] * n;
+        wt += (int64_t)rk[k] * n;
+        rsum += rk[k];
+      }
+    }
+    size_t fre = 0, tot = 0;
+    CK(cudaMemGetInfo(&fre, &tot));
+    const double need = 16.0 * (double)(ut + wt);
+    if (need > 0.8 * (double)fre) throw PlanError{FDH_ERR_MEMORY, "ACA factors do not fit in device memory"};
+    o->aca_U = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)ut));
+    o->aca_W = static_cast<double2*>(dalloc(sizeof(double2) * (size_t)wt));
+    o->aca_uoff = static_cast<int64_t*>(dalloc(sizeof(int64_t) * (size_t)nkeys));
+    o->aca_woff = static_cast<int64_t*>(dalloc(sizeof(int64_t) * (size_t)nkeys));
+    CK(cudaMemcpy(o->aca_uoff, uo.data(), sizeof(int64_t) * nkeys, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(o->aca_woff, wo.data(), sizeof(int64_t) * nkeys, cudaMemcpyHostToDevice));
+    // pass 1: the factors (same pivots) at their offsets; dense keys: W = A
+    for (int64_t k0 = 0; k0 < nkeys; k0 += chunk)
+      launch_aca_factor(o->st, o->dC, o->dirtab, k0, std::min(chunk, nkeys - k0), o->key_level, o->key_d, o->key_dir,
+                        eps, n, 1, o->aca_rank, nullptr, o->aca_uoff, o->aca_woff, o->aca_U, o->aca_W);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(o->st));
+    o->aca_bytes = (int64_t)need;
+    o->aca_mean_rank = nkeys > nd ? (double)rsum / (double)(nkeys - nd) : 0.0;
+    o->stats.aca_dense_keys = nd;
+    o->aca_eps = eps;
+  });
+}
+
 int fdh_sync(fdh_op* o) {
   if (!o) return fail(FDH_ERR_ARG, "NULL op");
   if (!o->parts.empty())
@@ -1197,6 +1325,9 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->graph_replays = o->graph_replays;
   s->apply_ms_sum = o->apply_ms_sum;
   s->applies_collected = o->applies_collected;
+  s->aca_eps = o->aca_eps;
+  s->aca_mean_rank = o->aca_mean_rank;
+  s->aca_bytes = o->aca_bytes;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

@@ -96,4 +96,27 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
                       int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs = 1);
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a);
 
+// ---- k_aca.cu: ACA-compressed coupling (opt-in, lossy)
+struct M2LAcaArgs {
+  int n_item = 0;
+  const int32_t *item_tile = nullptr, *item_seq = nullptr;
+  const int64_t *item_k0 = nullptr, *item_k1 = nullptr;
+  const int32_t *tile_nitem = nullptr, *tile_tslot = nullptr, *tile_keys = nullptr, *tile_src = nullptr;
+  const uint8_t *tile_cols = nullptr, *tile_cnt = nullptr;
+  const int32_t* rank = nullptr;  // per key: ACA rank, -1 = dense (W = A, U = I)
+  const int64_t *uoff = nullptr, *woff = nullptr;
+  const double2 *U = nullptr, *W = nullptr;
+  const double* mom = nullptr;
+  double* tile_acc = nullptr;
+  int* ticket = nullptr;
+  double* loc = nullptr;
+  int* counter = nullptr;
+};
+// pass 0: ranks (scratch: nkeys x n (n + 1) complex); pass 1: factors at uoff / woff
+void launch_aca_factor(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
+                       const int32_t* key_level, const int64_t* key_d, const int32_t* key_dir, double eps, int n,
+                       int pass, int32_t* rank, double2* scratch, const int64_t* uoff, const int64_t* woff,
+                       double2* Uall, double2* Wall);
+int launch_m2l_aca(cudaStream_t st, int n, int n_pad, int tile, const M2LAcaArgs& a);
+
 }  // namespace fdhelm

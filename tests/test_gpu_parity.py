@@ -385,3 +385,29 @@ def test_high_degrees(m):
     err = oracle.rel_l2(y, yo)
     print(f"m={m}: rel l2 vs oracle {err:.2e}")
     assert err <= TOL
+
+
+@pytest.mark.parametrize("m", [4, 5, 6])
+def test_aca_compressed_m2l(m):
+    """ACA-compressed coupling on the B200 (fdh_set_aca, lossy):
+    at eps = 1e-8 the apply agrees with the exact one and with the oracle's ACA
+    and dense matvecs to 1e-6; eps = 0 restores the exact M2L."""
+    c = CONFIGS[1]
+    tg, sr, q = make_inputs(c, nt=6000 if m == 6 else 10000, ns=5000 if m == 6 else 10000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32 if m > 4 else c.n_max, m, c.eta2, c.l_hf)
+    op = F.DirectionalOperator(*args)
+    y = op.apply(q)
+    op.set_aca(1e-8)
+    st = op.stats()
+    ya = op.apply(q)
+    o = oracle.Oracle(*args)
+    yo = o.apply(q)
+    o.set_aca(1e-8)
+    yoa = o.apply(q)
+    e1, e2, e3 = oracle.rel_l2(ya, y), oracle.rel_l2(ya, yo), oracle.rel_l2(ya, yoa)
+    print(f"m={m}: ACA mean rank {st['aca_mean_rank']:.1f} (dense keys {st['aca_dense_keys']}), vs exact {e1:.2e}, "
+          f"vs oracle {e2:.2e}, vs oracle ACA {e3:.2e}")
+    assert st["aca_eps"] == 1e-8 and st["aca_bytes"] > 0
+    assert e1 <= 1e-6 and e2 <= 1e-6 and e3 <= 1e-6
+    op.set_aca(0.0)
+    assert np.array_equal(op.apply(q), y)

@@ -251,3 +251,34 @@ def test_sampled_structure_oracle_matches_full(cfg, m):
     rows2, ys = samp.apply_sampled(q, leaves)
     assert np.array_equal(rows, rows2)
     assert np.array_equal(yf, ys)
+
+
+# ------------------------------------------------------ ACA
+def test_aca_spec_examples():
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    v = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    A = np.outer(u, v)
+    U, W = oracle.aca_compress(A, 1e-10)
+    assert U.shape[1] == 1 and np.linalg.norm(A - U @ W) <= 1e-14 * np.linalg.norm(A)  # rank 1 recovered
+    assert oracle.aca_compress(np.eye(30, dtype=np.complex128), 1e-12) is None  # incompressible: dense
+    # a k = 5 (PAPER section 4 grid) coupling matrix at eps = 1e-6 -> residual <= 1e-5
+    A = oracle.coupling_matrix(4, 3.2, (2 / 32, 2 / 32, 2 / 32), (2, 1, 0), oracle.dir_vector(1, 1, 0))
+    U, W = oracle.aca_compress(A, 1e-6)
+    assert U.shape[1] < 125 / 2 and np.linalg.norm(A - U @ W) <= 1e-5 * np.linalg.norm(A)
+
+
+def test_aca_matvec_agrees_with_dense():
+    """with ACA at eps = 1e-8 the matvec agrees with the dense one to 1e-6."""
+    c = CONFIGS[1]
+    tg, sr, q = make_inputs(c)
+    o = oracle.Oracle(tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
+    y = o.apply(q)
+    o.set_aca(1e-8)
+    r = o.aca_ranks()
+    assert (r > 0).sum() > 0 and r.max() < 125 // 2 + 1
+    ya = o.apply(q)
+    err = oracle.rel_l2(ya, y)
+    assert 0 < err <= 1e-6, err
+    o.set_aca(0.0)
+    assert np.array_equal(o.apply(q), y)
