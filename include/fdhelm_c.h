@@ -98,6 +98,7 @@ typedef struct fdh_stats {
   double aca_mean_rank;         /* mean ACA rank over the compressed keys                  */
   int64_t aca_bytes;            /* device bytes of the ACA factors                         */
   int64_t aca_dense_keys;       /* keys kept dense (2 k n >= n^2)                          */
+  int64_t nf_cache_bytes;       /* device bytes of the cached near-field kernel values     */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table
@@ -164,6 +165,14 @@ int fdh_apply_device(fdh_op* op, const double* x_dev, double* y_dev, void* strea
  * not to 1e-12.  eps = 0 returns to the exact M2L.  n <= 384 (m <= 6), nrhs = 1;
  * FDH_ERR_MEMORY when the factors do not fit in device memory. */
 int fdh_set_aca(fdh_op* op, double eps);
+/* Caches for repeated applies (PAPER.md:659, SPEC.md:519
+ * "a flag to cache them").  FDH_CACHE_NEARFIELD: the kernel value of every
+ * near-field pair (16 B per pair, M_D pairs) is computed once here and later
+ * applies stream it instead of recomputing it (exact: the reference's operation
+ * order and the library sincos).  FDH_ERR_MEMORY if it does not fit in device
+ * memory (configs >= 3), FDH_ERR_DOMAIN for a singular pair.  flags = 0 frees it. */
+#define FDH_CACHE_NEARFIELD 1
+int fdh_set_cache(fdh_op* op, int flags);
 /* Wait for the operator's applies and return (and clear) the deferred device
  * error of the fdh_apply_device calls since the last fdh_sync. */
 int fdh_sync(fdh_op* op);

@@ -25,9 +25,10 @@ LIB_PATH = os.environ.get("FDHELM_LIB") or os.path.join(HERE, "libfdhelm_b200.so
 LHF_DEFAULT = -2
 
 ERR_ARG, ERR_DOMAIN, ERR_DIM, ERR_UNSUPPORTED, ERR_CUDA, ERR_MEMORY = 1, 2, 3, 4, 5, 6
+CACHE_NEARFIELD = 1
 PHASES = ["h2d", "s2m", "m2m", "m2l", "l2l", "l2t", "p2p", "d2h"]
 SYMBOLS = ["fdh_create", "fdh_create_shard", "fdh_create_multi", "fdh_plan_only", "fdh_apply", "fdh_apply_multi",
-           "fdh_apply_device", "fdh_sync", "fdh_set_aca", "fdh_stream",
+           "fdh_apply_device", "fdh_sync", "fdh_set_aca", "fdh_set_cache", "fdh_stream",
            "fdh_set_timing", "fdh_get_stats", "fdh_export_tree", "fdh_export_perm", "fdh_export_lplus",
            "fdh_export_lminus", "fdh_export_dirsets", "fdh_export_owned_leaves", "fdh_structure_digest", "fdh_destroy", "fdh_last_error", "fdh_version",
            "fdh_fp64_peak_tflops", "fdh_tensor_peak_tops"]
@@ -46,7 +47,8 @@ class FdhStats(C.Structure):
                 ("w_segments", C.c_int64), ("m2l_impl", C.c_int64), ("m2l_i8_ops", C.c_int64),
                 ("nrhs", C.c_int64), ("hbm_bytes", C.c_int64 * 4), ("graph_replays", C.c_int64),
                 ("apply_ms_sum", C.c_double), ("applies_collected", C.c_int64), ("aca_eps", C.c_double),
-                ("aca_mean_rank", C.c_double), ("aca_bytes", C.c_int64), ("aca_dense_keys", C.c_int64)]
+                ("aca_mean_rank", C.c_double), ("aca_bytes", C.c_int64), ("aca_dense_keys", C.c_int64),
+                ("nf_cache_bytes", C.c_int64)]
 
 
 class FdhError(RuntimeError):
@@ -84,6 +86,7 @@ def lib():
         L.fdh_apply_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.fdh_sync.argtypes = [C.c_void_p]
         L.fdh_set_aca.argtypes = [C.c_void_p, C.c_double]
+        L.fdh_set_cache.argtypes = [C.c_void_p, C.c_int]
         L.fdh_stream.argtypes = [C.c_void_p]
         L.fdh_stream.restype = C.c_void_p
         L.fdh_set_timing.argtypes = [C.c_void_p, C.c_int]
@@ -188,6 +191,11 @@ class DirectionalOperator:
         """ACA-compressed coupling (lossy, opt-in): eps > 0 factorises
         the coupling matrices on the device, eps = 0 returns to the exact M2L."""
         _chk(lib().fdh_set_aca(self.h, float(eps)))
+
+    def set_cache(self, nearfield=True):
+        """Cache the near-field kernel values for repeated applies (fdh_set_cache,
+        SPEC.md:519); False frees the cache."""
+        _chk(lib().fdh_set_cache(self.h, CACHE_NEARFIELD if nearfield else 0))
 
     def sync(self):
         """Wait for the device-path applies; raises their deferred device error

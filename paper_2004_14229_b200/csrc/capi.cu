@@ -175,6 +175,11 @@ struct fdh_op {
   std::vector<void*> aca_allocs;
   int64_t aca_bytes = 0;
   double aca_mean_rank = 0.0;
+  // cached near-field kernel values (fdh_set_cache FDH_CACHE_NEARFIELD)
+  int64_t* nf_koff = nullptr;
+  double2* nf_K = nullptr;
+  std::vector<void*> nf_allocs;
+  int64_t nf_bytes = 0;
   // multi-GPU operator (fdh_create with n_gpus > 1): one target-leaf shard per
   // device (rank g of n_gpus on device g), y reduced to device 0 over NCCL
   std::vector<fdh_op*> parts;
@@ -192,6 +197,7 @@ struct fdh_op {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (void* p : allocs) cudaFree(p);
     for (void* p : aca_allocs) cudaFree(p);
+    for (void* p : nf_allocs) cudaFree(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : ev_all)
@@ -534,9 +540,13 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   // each M2L CTA, different pipes); measured no faster.
   auto near_field = [&](cudaStream_t snf, int grid) {
     rec(o, FDH_NPHASES + 3, snf);
-    launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
-               o->tz, o->sx, o->sy, o->sz, o->q4, o->diag_slot, nullptr, P.prm.zero_diagonal, o->ynear, o->flag,
-               o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt, grid);
+    if (o->nf_K)
+      launch_p2p_cached(snf, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->nf_koff,
+                        o->nf_K, o->q, o->ynear, R, o->ns, o->nt);
+    else
+      launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
+                 o->tz, o->sx, o->sy, o->sz, o->q4, o->diag_slot, nullptr, P.prm.zero_diagonal, o->ynear, o->flag,
+                 o->kappa * P.nf_max_dist, o->sctab, R, o->ns, o->nt, grid);
     L += (o->n_leaf > 0) * p2p_launches(R);
     rec(o, FDH_NPHASES + 4, snf);
   };
@@ -1212,6 +1222,76 @@ int fdh_set_aca(fdh_op* o, double eps) {
   });
 }
 
+int fdh_set_cache(fdh_op* o, int flags) {
+  if (!o) return fail(FDH_ERR_ARG, "NULL op");
+  for (fdh_op* p : o->parts) {
+    cudaSetDevice(p->device);
+    if (const int rc = fdh_set_cache(p, flags)) return rc;
+  }
+  if (!o->parts.empty()) {
+    cudaSetDevice(0);
+    return FDH_OK;
+  }
+  if (!o->st) return fail(FDH_ERR_UNSUPPORTED, "operator was built with fdh_plan_only (no device state)");
+  return guard([&] {
+    CK(cudaSetDevice(o->device));
+    CK(cudaStreamSynchronize(o->st));
+    for (void* p : o->nf_allocs) cudaFree(p);
+    o->nf_allocs.clear();
+    o->nf_K = nullptr;
+    o->nf_koff = nullptr;
+    o->nf_bytes = 0;
+    o->gx = nullptr;  // re-capture the apply graph
+    if (o->gexec) {
+      CK(cudaGraphExecDestroy(o->gexec));
+      o->gexec = nullptr;
+    }
+    if (!(flags & FDH_CACHE_NEARFIELD)) return;
+    const Plan& P = o->P;
+    const int64_t ne = (int64_t)P.l2t_begin.size();
+    std::vector<int64_t> koff(ne + 1, 0);
+    for (int64_t e = 0; e < ne; ++e) {
+      int64_t ns = 0;
+      for (int64_t r = P.p2p_ptr[e]; r < P.p2p_ptr[e + 1]; ++r) ns += P.p2p_send[r] - P.p2p_sbeg[r];
+      koff[e + 1] = koff[e] + ns * (int64_t)(P.l2t_end[e] - P.l2t_begin[e]);
+    }
+    size_t fre = 0, tot = 0;
+    CK(cudaMemGetInfo(&fre, &tot));
+    const double need = 16.0 * (double)koff[ne];
+    if (need > 0.7 * (double)fre)
+      throw PlanError{FDH_ERR_MEMORY, "near-field cache (" + std::to_string((long long)(need / 1e9)) +
+                                          " GB) does not fit in device memory"};
+    void* pk = nullptr;
+    void* pK = nullptr;
+    if (cudaMalloc(&pk, sizeof(int64_t) * (ne + 1)) != cudaSuccess ||
+        cudaMalloc(&pK, std::max<size_t>(16, (size_t)need)) != cudaSuccess) {
+      if (pk) cudaFree(pk);
+      throw PlanError{FDH_ERR_MEMORY, "near-field cache allocation failed"};
+    }
+    o->nf_allocs = {pk, pK};
+    o->nf_koff = static_cast<int64_t*>(pk);
+    o->nf_K = static_cast<double2*>(pK);
+    CK(cudaMemcpy(o->nf_koff, koff.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemset(o->flag, 0, sizeof(int)));
+    launch_p2p_cache_fill(o->st, o->kappa, (int)ne, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send,
+                          o->tx, o->ty, o->tz, o->sx, o->sy, o->sz, o->diag_slot, P.prm.zero_diagonal, o->nf_koff,
+                          o->nf_K, o->flag);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(o->st));
+    int f = 0;
+    CK(cudaMemcpy(&f, o->flag, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(o->flag, 0, sizeof(int)));
+    if (f & 1) {
+      for (void* p : o->nf_allocs) cudaFree(p);
+      o->nf_allocs.clear();
+      o->nf_K = nullptr;
+      o->nf_koff = nullptr;
+      throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
+    }
+    o->nf_bytes = (int64_t)need;
+  });
+}
+
 int fdh_sync(fdh_op* o) {
   if (!o) return fail(FDH_ERR_ARG, "NULL op");
   if (!o->parts.empty())
@@ -1328,6 +1408,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->aca_eps = o->aca_eps;
   s->aca_mean_rank = o->aca_mean_rank;
   s->aca_bytes = o->aca_bytes;
+  s->nf_cache_bytes = o->nf_bytes;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

@@ -411,3 +411,34 @@ def test_aca_compressed_m2l(m):
     assert e1 <= 1e-6 and e2 <= 1e-6 and e3 <= 1e-6
     op.set_aca(0.0)
     assert np.array_equal(op.apply(q), y)
+
+
+def test_cached_near_field():
+    """FDH_CACHE_NEARFIELD (fdh_set_cache): the near-field kernel values
+    cached once, streamed by later applies -- the same y as recomputing them (to the
+    sincos / rsqrt rounding) and the oracle; zero diagonal, several right-hand sides,
+    and freeing the cache restore the computing kernel bitwise."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000, ns=25000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, 4, c.eta2, c.l_hf)
+    op = F.DirectionalOperator(*args)
+    y = op.apply(q)
+    op.set_cache(True)
+    st = op.stats()
+    assert st["nf_cache_bytes"] == 16 * st["m_d"]
+    yc = op.apply(q)
+    assert oracle.rel_l2(yc, y) <= 1e-13
+    assert oracle.rel_l2(yc, oracle.Oracle(*args).apply(q)) <= TOL
+    op.set_cache(False)
+    assert np.array_equal(op.apply(q), y)
+    rng = np.random.default_rng(4)
+    pts = [rng.random(8000) for _ in range(3)]
+    X = rng.standard_normal((3, 8000)) + 1j * rng.standard_normal((3, 8000))
+    opz = F.DirectionalOperator(pts, pts, (0, 0, 0), (1, 1, 1), 10.0, 32, 4, 1.0, -2, 30, True, nrhs=4)
+    Y = opz.apply_multi(X)
+    opz.set_cache(True)
+    assert oracle.rel_l2(opz.apply_multi(X), Y) <= 1e-13
+    ops = F.DirectionalOperator(pts, pts, (0, 0, 0), (1, 1, 1), 10.0, 32, 4)
+    with pytest.raises(F.FdhError) as e:
+        ops.set_cache(True)  # coincident points without the zero diagonal: singular
+    assert e.value.code == F.ERR_DOMAIN

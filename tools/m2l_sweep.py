@@ -53,6 +53,10 @@ def main():
             try:
                 t = time.perf_counter()
                 op = F.DirectionalOperator(*args)
+                if os.environ.get("FDH_CACHE_NF") == "1":
+                    op.set_cache(True)  # cached near-field kernel values (fdh_set_cache)
+                if os.environ.get("FDH_ACA_EPS"):
+                    op.set_aca(float(os.environ["FDH_ACA_EPS"]))  # ACA-compressed coupling (lossy)
                 setup = time.perf_counter() - t
                 op.apply(q)  # warm-up (graph capture)
                 op.set_timing(True)
