@@ -31,6 +31,7 @@ struct Params {
   int depth_cap = 30;
   bool zero_diagonal = false;
   int nrhs = 1;            // right-hand sides per device batch (power of two, <= 16)
+  int n_gpus = 1;          // > 1: one process drives devices 0..n_gpus-1 (target shards, NCCL reduce of y)
 };
 
 inline void check(int rc) {
@@ -77,9 +78,16 @@ class DirectionalOperator {
       : nt_(tx.size()), ns_(sx.size()) {
     if (ty.size() != nt_ || tz.size() != nt_ || sy.size() != ns_ || sz.size() != ns_)
       throw std::invalid_argument("coordinate arrays of one point set differ in length");
-    check(fdh_create_multi(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(),
-                           (int64_t)ns_, root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap,
-                           p.zero_diagonal ? 1 : 0, 0, 1, p.nrhs, &op_));
+    if (p.n_gpus > 1) {
+      if (p.nrhs != 1) throw std::invalid_argument("n_gpus > 1 takes one right-hand side per apply");
+      check(fdh_create(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(), (int64_t)ns_,
+                       root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap, p.zero_diagonal ? 1 : 0,
+                       p.n_gpus, &op_));
+    } else {
+      check(fdh_create_multi(tx.data(), ty.data(), tz.data(), (int64_t)nt_, sx.data(), sy.data(), sz.data(),
+                             (int64_t)ns_, root_lo, root_hi, p.kappa, p.n_max, p.m, p.eta2, p.l_hf, p.depth_cap,
+                             p.zero_diagonal ? 1 : 0, 0, 1, p.nrhs, &op_));
+    }
   }
   DirectionalOperator(const DirectionalOperator&) = delete;
   DirectionalOperator& operator=(const DirectionalOperator&) = delete;
@@ -108,6 +116,15 @@ class DirectionalOperator {
     return s;
   }
   fdh_op* handle() { return op_; }
+  // options for repeated applies: ACA-compressed coupling (lossy, SPEC.md:440-448;
+  // eps = 0 -> exact) and the cached near-field kernel values
+  void set_aca(double eps) { check(fdh_set_aca(op_, eps)); }
+  void set_cache_nearfield(bool on) { check(fdh_set_cache(op_, on ? FDH_CACHE_NEARFIELD : 0)); }
+  // device-resident apply (x_dev, y_dev: device pointers; errors deferred to sync())
+  void apply_device(const Complex* x_dev, Complex* y_dev, void* stream = nullptr) {
+    check(fdh_apply_device(op_, reinterpret_cast<const double*>(x_dev), reinterpret_cast<double*>(y_dev), stream));
+  }
+  void sync() { check(fdh_sync(op_)); }
 
   // canonical introspection (int64 rows, see fdhelm_c.h): the cluster trees
   // (level, i, j, k, begin, end, leaf), slot -> original index permutations,

@@ -493,8 +493,8 @@ void build_m2l(Plan& P) {
   // column of (slot i of the tile, rhs r) is i * R + r and refers to the
   // rhs-major slot id r * nslots + slot (moments / locals stored per rhs)
   const int R = P.prm.nrhs;
-  if (R < 1 || R > std::abs(TT) || std::abs(TT) % R != 0)
-    throw PlanError{1, "nrhs must divide the M2L tile width " + std::to_string(std::abs(TT))};
+  const int tw = TT < 0 ? 16 : TT;  // auto: both candidates (16, 32) are multiples of R <= 16
+  if (R < 1 || R > tw || tw % R != 0) throw PlanError{1, "nrhs must divide the M2L tile width " + std::to_string(tw)};
   // pairs (target slot, key, source slot) grouped by target slot: parallel
   // counting pass, prefix, parallel scatter with atomic cursors (the order
   // inside a slot is then fixed by the per-slot sort by key -- keys are unique
