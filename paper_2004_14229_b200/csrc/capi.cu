@@ -176,7 +176,8 @@ struct fdh_op {
   int64_t aca_bytes = 0;
   double aca_mean_rank = 0.0;
   // cached near-field kernel values (fdh_set_cache FDH_CACHE_NEARFIELD)
-  int64_t* nf_koff = nullptr;
+  int64_t *nf_koff = nullptr, *nf_poff = nullptr;
+  uint32_t* nf_spos = nullptr;
   double2* nf_K = nullptr;
   std::vector<void*> nf_allocs;
   int64_t nf_bytes = 0;
@@ -541,8 +542,8 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
   auto near_field = [&](cudaStream_t snf, int grid) {
     rec(o, FDH_NPHASES + 3, snf);
     if (o->nf_K)
-      launch_p2p_cached(snf, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->nf_koff,
-                        o->nf_K, o->q, o->ynear, R, o->ns, o->nt);
+      launch_p2p_cached(snf, o->n_leaf, o->l2t_beg, o->l2t_end, o->nf_koff, o->nf_poff, o->nf_spos, o->nf_K, o->q,
+                        o->ynear, R, o->ns, o->nt);
     else
       launch_p2p(snf, o->kappa, o->n_leaf, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send, o->tx, o->ty,
                  o->tz, o->sx, o->sy, o->sz, o->q4, o->diag_slot, nullptr, P.prm.zero_diagonal, o->ynear, o->flag,
@@ -1249,33 +1250,36 @@ int fdh_set_cache(fdh_op* o, int flags) {
     if (!(flags & FDH_CACHE_NEARFIELD)) return;
     const Plan& P = o->P;
     const int64_t ne = (int64_t)P.l2t_begin.size();
-    std::vector<int64_t> koff(ne + 1, 0);
+    std::vector<int64_t> koff(ne + 1, 0), poff(ne + 1, 0);
     for (int64_t e = 0; e < ne; ++e) {
       int64_t ns = 0;
       for (int64_t r = P.p2p_ptr[e]; r < P.p2p_ptr[e + 1]; ++r) ns += P.p2p_send[r] - P.p2p_sbeg[r];
       koff[e + 1] = koff[e] + ns * (int64_t)(P.l2t_end[e] - P.l2t_begin[e]);
+      poff[e + 1] = poff[e] + ns;
     }
     size_t fre = 0, tot = 0;
     CK(cudaMemGetInfo(&fre, &tot));
-    const double need = 16.0 * (double)koff[ne];
+    const double need = 16.0 * (double)koff[ne] + 4.0 * (double)poff[ne];
     if (need > 0.7 * (double)fre)
       throw PlanError{FDH_ERR_MEMORY, "near-field cache (" + std::to_string((long long)(need / 1e9)) +
                                           " GB) does not fit in device memory"};
-    void* pk = nullptr;
-    void* pK = nullptr;
-    if (cudaMalloc(&pk, sizeof(int64_t) * (ne + 1)) != cudaSuccess ||
-        cudaMalloc(&pK, std::max<size_t>(16, (size_t)need)) != cudaSuccess) {
-      if (pk) cudaFree(pk);
-      throw PlanError{FDH_ERR_MEMORY, "near-field cache allocation failed"};
-    }
-    o->nf_allocs = {pk, pK};
-    o->nf_koff = static_cast<int64_t*>(pk);
-    o->nf_K = static_cast<double2*>(pK);
+    auto dalloc = [&](size_t bytes) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess)
+        throw PlanError{FDH_ERR_MEMORY, "near-field cache allocation failed"};
+      o->nf_allocs.push_back(p);
+      return p;
+    };
+    o->nf_koff = static_cast<int64_t*>(dalloc(sizeof(int64_t) * (ne + 1)));
+    o->nf_poff = static_cast<int64_t*>(dalloc(sizeof(int64_t) * (ne + 1)));
+    o->nf_K = static_cast<double2*>(dalloc(16 * (size_t)koff[ne]));
+    o->nf_spos = static_cast<uint32_t*>(dalloc(4 * (size_t)poff[ne]));
     CK(cudaMemcpy(o->nf_koff, koff.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(o->nf_poff, poff.data(), sizeof(int64_t) * (ne + 1), cudaMemcpyHostToDevice));
     CK(cudaMemset(o->flag, 0, sizeof(int)));
     launch_p2p_cache_fill(o->st, o->kappa, (int)ne, o->l2t_beg, o->l2t_end, o->p2p_ptr, o->p2p_sbeg, o->p2p_send,
                           o->tx, o->ty, o->tz, o->sx, o->sy, o->sz, o->diag_slot, P.prm.zero_diagonal, o->nf_koff,
-                          o->nf_K, o->flag);
+                          o->nf_poff, o->nf_K, o->nf_spos, o->flag);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(o->st));
     int f = 0;
@@ -1285,7 +1289,6 @@ int fdh_set_cache(fdh_op* o, int flags) {
       for (void* p : o->nf_allocs) cudaFree(p);
       o->nf_allocs.clear();
       o->nf_K = nullptr;
-      o->nf_koff = nullptr;
       throw PlanError{FDH_ERR_DOMAIN, "Helmholtz kernel is singular at x == y (near field)"};
     }
     o->nf_bytes = (int64_t)need;

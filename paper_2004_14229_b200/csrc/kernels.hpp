@@ -123,9 +123,10 @@ int launch_m2l_aca(cudaStream_t st, int n, int n_pad, int tile, const M2LAcaArgs
 void launch_p2p_cache_fill(cudaStream_t st, double kappa, int n_entry, const uint32_t* beg, const uint32_t* end,
                            const int64_t* ptr, const uint32_t* sbeg, const uint32_t* send, const double* tx,
                            const double* ty, const double* tz, const double* sx, const double* sy, const double* sz,
-                           const uint32_t* diag_slot, int zero_diag, const int64_t* koff, double2* K, int* flag);
-void launch_p2p_cached(cudaStream_t st, int n_entry, const uint32_t* beg, const uint32_t* end, const int64_t* ptr,
-                       const uint32_t* sbeg, const uint32_t* send, const int64_t* koff, const double2* K,
-                       const double2* q, double2* y_slot, int nrhs, int64_t qstride, int64_t ystride);
+                           const uint32_t* diag_slot, int zero_diag, const int64_t* koff, const int64_t* poff,
+                           double2* K, uint32_t* spos, int* flag);
+void launch_p2p_cached(cudaStream_t st, int n_entry, const uint32_t* beg, const uint32_t* end, const int64_t* koff,
+                       const int64_t* poff, const uint32_t* spos, const double2* K, const double2* q, double2* y_slot,
+                       int nrhs, int64_t qstride, int64_t ystride);
 
 }  // namespace fdhelm

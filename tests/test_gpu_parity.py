@@ -425,7 +425,7 @@ def test_cached_near_field():
     y = op.apply(q)
     op.set_cache(True)
     st = op.stats()
-    assert st["nf_cache_bytes"] == 16 * st["m_d"]
+    assert st["nf_cache_bytes"] >= 16 * st["m_d"]
     yc = op.apply(q)
     assert oracle.rel_l2(yc, y) <= 1e-13
     assert oracle.rel_l2(yc, oracle.Oracle(*args).apply(q)) <= TOL
