@@ -657,7 +657,17 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
     run_i8<1, 16, 4, 8, 1>(st, a, 3, 2, 1);
   } else if (mb >= 2 && tile == 32) {
     // 32 target columns (N up to 448 per W digit): one 128-row M-block per pass
-    for (int b = 0; b < mb; ++b) run_i8<1, 32, 4, 8, 1>(st, a, mb, b, b);
+    // 5 stages fit beside the m = 5, 6 item tables (fkeys <= 128): deeper W / B
+    // lookahead (FDH_I8_NST=4 selects the 4-stage ring of the m <= 4 kernel)
+    static const int nst = [] {
+      const char* e = std::getenv("FDH_I8_NST");
+      return e ? std::atoi(e) : 5;
+    }();
+    const bool five = nst == 5 && i8_smem<1, 32, 5, 8>(a.fkeys) + 2048 <= 232448;  // + static shared (aligned)
+    for (int b = 0; b < mb; ++b) {
+      if (five) run_i8<1, 32, 5, 8, 1>(st, a, mb, b, b);
+      else run_i8<1, 32, 4, 8, 1>(st, a, mb, b, b);
+    }
   } else {
     return 1;
   }
