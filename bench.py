@@ -324,13 +324,14 @@ def run_ours(args, c, rank, world, local_rank):
         stream.synchronize()
         return ev_a[0].elapsed_time(ev_a[1])
 
+    op.set_timing(True)  # phase events as event-record nodes inside the graph (captured in the warm-up)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     op.sync()  # deferred device errors of the warm-up (fdh_sync)
     if world > 1:
         dist.barrier()
-    op.set_timing(True)  # phase events as event-record nodes inside the graph replays
+    op.set_timing(True)  # reset the averages: only the timed applies below count (same graph, no re-capture)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     dev_ms = []
     torch.cuda.synchronize()
