@@ -126,7 +126,12 @@ struct fdh_op {
   struct Seg {
     int item0, item1;
     int64_t key0, key1;
+    bool gen = true;  // generate the segment's W digits (on-the-fly mode; pair-mode sub-segments share them)
   };
+  // int8 pair mode (P.m2l_pair): per-pair output buffer of one segment, the per-slot
+  // pair lists and their cursors
+  double* pair_out = nullptr;
+  int64_t *red_ptr = nullptr, *red_idx = nullptr, *red_cur = nullptr;
   std::vector<Seg> segs;
   int64_t w_slot_keys = 0;
   double2* sctab = nullptr;  // (sin, cos)(i pi / 256), i < 512: near-field table sincos
@@ -387,7 +392,8 @@ void setup_device(fdh_op* o) {
   const int64_t R = o->R = P.prm.nrhs;
   o->mom = o->alloc<double>((size_t)(R * P.S.nslots * np2));  // [rhs][slot][Re | Im]
   o->loc = o->alloc<double>((size_t)(R * P.T.nslots * np2));
-  o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
+  if (!P.m2l_pair)  // chained tile accumulators (pair mode: one key per item, no chains)
+    o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
   o->ticket = o->alloc<int>((size_t)std::max(
       (P.prm.m2l_impl == 1 ? m2l_i8_passes(P.n, P.prm.tile) : 1) * o->n_tile, 1));  // one chain per M-block pass
   o->q = o->alloc<double2>((size_t)(R * o->ns));
@@ -466,6 +472,25 @@ void setup_device(fdh_op* o) {
       const int64_t slot_keys = make_segments(wkq);
       o->Wq = o->alloc<int8_t>((size_t)(2 * slot_keys * wkq));
       CK(cudaMemsetAsync(o->Wq, 0, (size_t)(2 * slot_keys * wkq), o->st));  // padding rows / K stay zero
+    }
+    if (P.m2l_pair) {
+      // pair mode: segments of at most pair_cap pairs (the output buffer), cut inside
+      // the W segments when the digits are generated per apply
+      CK(cudaMemGetInfo(&fre, &tot));
+      double cap_bytes = std::min(8.0e9, 0.25 * (double)fre);
+      if (const char* pb = std::getenv("FDH_PAIR_OUT_MB")) cap_bytes = std::max(1.0, std::atof(pb)) * 1048576.0;
+      const int64_t TT = P.prm.tile;
+      const int64_t cap_items = std::max<int64_t>(1, (int64_t)(cap_bytes / (16.0 * P.n_pad * TT)));
+      std::vector<fdh_op::Seg> base = o->segs;
+      if (base.empty()) base.push_back({0, (int)P.item_tile.size(), 0, nkeys, true});
+      o->segs.clear();
+      for (const fdh_op::Seg& b : base)
+        for (int i = b.item0; i < b.item1; i += (int)cap_items)
+          o->segs.push_back({i, (int)std::min<int64_t>(b.item1, i + cap_items), b.key0, b.key1, i == b.item0});
+      o->pair_out = o->alloc<double>((size_t)(cap_items * TT * 2 * P.n_pad));
+      o->red_ptr = o->up(P.red_ptr);
+      o->red_idx = o->up(P.red_idx);
+      o->red_cur = o->alloc<int64_t>((size_t)std::max<int64_t>(1, P.T.nslots));
     }
     o->counter = o->alloc<int>((size_t)(m2l_i8_passes(P.n, P.prm.tile) * std::max<size_t>(1, o->segs.size())));
     CK(cudaGetLastError());
@@ -622,7 +647,37 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.counter = o->counter;
     const int ng = npass;
     rec(o, FDH_NPHASES + 1, st);
-    if (o->w_resident) {
+    if (P.m2l_pair) {
+      // pair mode: per segment the key-major M2L into the pair buffer, then the
+      // per-slot reduction into the locals (pair order = key order)
+      CK(cudaMemcpyAsync(o->red_cur, o->red_ptr, sizeof(int64_t) * (size_t)P.T.nslots, cudaMemcpyDeviceToDevice, st));
+      const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
+      int wslot = -1;
+      for (size_t sg = 0; sg < o->segs.size(); ++sg) {
+        const auto& S = o->segs[sg];
+        M2LI8Args b = a;
+        b.item0 = S.item0;
+        b.n_item = S.item1 - S.item0;
+        b.counter = o->counter + sg * npass;
+        b.pair_out = o->pair_out;
+        if (!o->w_resident) {
+          if (S.gen) {
+            wslot = (wslot + 1) & 1;
+            launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
+                               o->lvmax_w, o->Wq + (int64_t)wslot * o->w_slot_keys * wkq, n, o->nkq,
+                               m2l_i8_wgroup(n, P.prm.tile), S.key0);
+            L += 1;
+          }
+          b.Wq = o->Wq + (int64_t)wslot * o->w_slot_keys * wkq;
+          b.key_base = S.key0;
+        }
+        if (launch_m2l_i8(st, n, P.prm.tile, b) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+        launch_m2l_reduce(st, P.T.nslots, o->red_ptr, o->red_idx, o->red_cur, o->pair_out,
+                          (int64_t)S.item0 * P.prm.tile, (int64_t)S.item1 * P.prm.tile, o->loc, np);
+        L += ng + 1;
+      }
+      L += 3;
+    } else if (o->w_resident) {
       if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
       L += 2 + ng;
     } else {
@@ -1412,6 +1467,7 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->aca_mean_rank = o->aca_mean_rank;
   s->aca_bytes = o->aca_bytes;
   s->nf_cache_bytes = o->nf_bytes;
+  s->m2l_pair_mode = P.m2l_pair ? 1 : 0;
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;

@@ -325,7 +325,7 @@ __global__ void __maxnreg__(128)
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
              int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int fkeys, int mb_tot,
-             int blk0, int tick_off, int64_t key_base, int nrhs) {
+             int blk0, int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int NT = S::THREADS;
@@ -553,7 +553,13 @@ __global__ void __maxnreg__(128)
 #pragma unroll
           for (int e = 0; e < 8; ++e) v[e] += __ldcg(pa + e);
         }
-        if (last) {
+        if (pair_out) {  // pair mode: one key per item, the pair's values to the output buffer
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = 8 * g + e;
+            pair_out[((int64_t)idx * TT + (col >> 1)) * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
+          }
+        } else if (last) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int col = 8 * g + e;
@@ -606,7 +612,7 @@ void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass)
                                      a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
                                      a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.counter + pass, a.item0,
                                      a.n_item, a.nkq, a.n_pad, a.fkeys, mb_tot, blk0, pass * a.n_tile, a.key_base,
-                                     a.nrhs);
+                                     a.nrhs, a.pair_out);
 }
 
 }  // namespace
@@ -673,6 +679,33 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   }
   return 0;
 }
+namespace {
+// pair mode: loc[t] += sum of its pairs' outputs of this segment [p0, p1), in pair
+// order (cursor[t] advances through the slot's sorted pair list segment by segment)
+__global__ void __launch_bounds__(256) k_m2l_reduce(const int64_t* __restrict__ red_ptr,
+                                                    const int64_t* __restrict__ red_idx, int64_t* __restrict__ cursor,
+                                                    const double* __restrict__ out, int64_t p0, int64_t p1,
+                                                    double* __restrict__ loc, int n_pad) {
+  const int64_t t = blockIdx.x;
+  const int64_t c0 = cursor[t], c1 = red_ptr[t + 1];
+  if (c0 >= c1 || red_idx[c0] >= p1) return;
+  int64_t ce = c0;  // the slot's pairs in this segment: [c0, ce)
+  while (ce < c1 && red_idx[ce] < p1) ++ce;
+  for (int r = threadIdx.x; r < 2 * n_pad; r += blockDim.x) {
+    double a = 0.0;
+    for (int64_t c = c0; c < ce; ++c) a += out[(red_idx[c] - p0) * 2 * n_pad + r];
+    loc[t * 2 * n_pad + r] += a;
+  }
+  if (threadIdx.x == 0) cursor[t] = ce;
+}
+}  // namespace
+
+void launch_m2l_reduce(cudaStream_t st, int64_t nslots, const int64_t* red_ptr, const int64_t* red_idx,
+                       int64_t* cursor, const double* out, int64_t p0, int64_t p1, double* loc, int n_pad) {
+  if (nslots <= 0) return;
+  k_m2l_reduce<<<(unsigned)nslots, 256, 0, st>>>(red_ptr, red_idx, cursor, out, p0, p1, loc, n_pad);
+}
+
 int m2l_i8_passes(int n, int tile) {
   const int mb = (n + 127) / 128;
   if (tile == 32) return mb;

@@ -81,7 +81,10 @@ struct M2LI8Args {
   int nrhs = 1;          // moment scales per (rhs, level): lvmax_v[rhs * kMaxLevels + level];
                          // tile column c = (slot, rhs) with rhs = c % nrhs
   int* counter = nullptr;  // zeroed item-claim counters, one per M-block pass (persistent grid)
+  double* pair_out = nullptr;  // pair mode: per (item, column) the pair's 2 n_pad values
 };
+void launch_m2l_reduce(cudaStream_t st, int64_t nslots, const int64_t* red_ptr, const int64_t* red_idx,
+                       int64_t* cursor, const double* out, int64_t p0, int64_t p1, double* loc, int n_pad);
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
 int64_t m2l_i8_wbytes_per_key(int n, int nkq);

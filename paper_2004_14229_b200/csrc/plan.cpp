@@ -563,13 +563,17 @@ void build_m2l(Plan& P) {
   std::vector<int32_t> key_lo(64, 0), key_hi(64, 0);
   for (int32_t k = (int32_t)P.key_level.size() - 1; k >= 0; --k) key_lo[P.key_level[k]] = k;
   for (int32_t k = 0; k < (int32_t)P.key_level.size(); ++k) key_hi[P.key_level[k]] = k + 1;
-  if (TT < 0) {
+  bool pair_mode = false;
+  if (P.prm.m2l_impl == 1) {
     // int8 M2L with 2-3 M-blocks: 16 target columns (one pass over M-blocks {0,1}
     // [+ {2}]) or 32 (one pass per M-block: twice the columns per W byte, the
     // issued rate measured 1.14-1.18x higher, profiles/r02_m2l_sweep_tt_chunk.jsonl)
     // -- but the union of a wider tile's key lists leaves more columns absent
     // (clustered sources: config 5).  Estimated on every 8th 32-wide tile: the
     // tile-keys of it and of its two 16-wide halves; 32 when 32 K32 / 1.16 < 16 K16.
+    // When even the better tiling leaves most columns without a key (useful <
+    // 0.45: clustered sources), the M2L runs key-major on (target, source) PAIRS
+    // instead (pair mode below): every column carries a key.
     const int64_t w32 = 32 / R, w16 = 16 / R;
     std::vector<std::pair<int64_t, int64_t>> smp;  // [begin, end) into ts of sampled 32-wide tiles
     for (size_t i = 0; i < ts.size();) {
@@ -581,8 +585,8 @@ void build_m2l(Plan& P) {
         if ((q & 7) == 0) smp.push_back({(int64_t)k, (int64_t)std::min(j, k + w32)});
       i = j;
     }
-    int64_t k16 = 0, k32 = 0;
-#pragma omp parallel for schedule(dynamic, 16) reduction(+ : k16, k32)
+    int64_t k16 = 0, k32 = 0, pairs_s = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : k16, k32, pairs_s)
     for (int64_t si = 0; si < (int64_t)smp.size(); ++si) {
       const int64_t b = smp[si].first, e = smp[si].second;
       const int l = T.slot_level[ts[b]];
@@ -591,6 +595,7 @@ void build_m2l(Plan& P) {
       mk.assign(kr, 0);
       for (int64_t i = b; i < e; ++i) {
         const uint8_t bit = (i - b) < w16 ? 1 : 2;
+        pairs_s += (ptr[ts[i] + 1] - ptr[ts[i]]) * R;
         for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) mk[sk[q] - kb] |= bit;
       }
       for (int32_t k = 0; k < kr; ++k) {
@@ -598,11 +603,92 @@ void build_m2l(Plan& P) {
         k16 += (mk[k] & 1) + (mk[k] >> 1);
       }
     }
-    TT = (32.0 * (double)k32 / 1.16 < 16.0 * (double)k16) ? 32 : 16;
+    if (TT < 0) TT = (32.0 * (double)k32 / 1.16 < 16.0 * (double)k16) ? 32 : 16;
+    const double useful = (double)pairs_s / std::max(1.0, (double)(TT == 32 ? k32 : k16) * TT);
+    const char* pm = std::getenv("FDH_M2L_PAIR");  // 1: force pair mode, 0: never
+    pair_mode = R == 1 && (pm ? pm[0] == '1' : useful < 0.45);
+    if (pair_mode) TT = 32;
     P.prm.tile = TT;
     if (mdbg)
-      std::fprintf(stderr, "[m2l] tile width: sampled tile-keys 16: %lld, 32: %lld -> %d\n", (long long)k16,
-                   (long long)k32, TT);
+      std::fprintf(stderr, "[m2l] tile width: sampled tile-keys 16: %lld, 32: %lld, useful %.3f -> %d%s\n",
+                   (long long)k16, (long long)k32, useful, TT, pair_mode ? " (pair mode)" : "");
+  }
+  if (pair_mode) {
+    // ---- pair mode (key-major): the pairs (target slot, source slot) of every key,
+    // keys in id order, pairs of a key in target-slot order, cut into tiles of 32
+    // pairs; one item per tile (one key: no chains).  The kernel writes each pair's
+    // n values to an output buffer; k_m2l_reduce adds them to the locals per target
+    // slot in pair order (= key order): deterministic, no atomics.
+    std::vector<int64_t> kc(P.key_level.size() + 1, 0);
+    for (int32_t t : ts)
+      for (int64_t q = ptr[t]; q < ptr[t + 1]; ++q) ++kc[sk[q] + 1];
+    for (size_t k = 0; k + 1 < kc.size(); ++k) kc[k + 1] += kc[k];
+    const int64_t np = kc.back();
+    std::vector<int32_t> pt(np), ps(np);
+    {
+      std::vector<int64_t> cur(kc.begin(), kc.end() - 1);
+      std::vector<int32_t> tss(ts.begin(), ts.end());
+      std::sort(tss.begin(), tss.end());  // target-slot order inside a key
+      for (int32_t t : tss)
+        for (int64_t q = ptr[t]; q < ptr[t + 1]; ++q) {
+          const int64_t o = cur[sk[q]]++;
+          pt[o] = t;
+          ps[o] = ss[q];
+        }
+    }
+    int64_t ntile = 0;
+    for (size_t k = 0; k + 1 < kc.size(); ++k) ntile += (kc[k + 1] - kc[k] + TT - 1) / TT;
+    P.tile_level.assign(ntile, 0);
+    P.tile_dir.assign(ntile, 0);
+    P.tile_tslot.assign(ntile * TT, -1);
+    P.tile_kptr.assign(ntile + 1, 0);
+    P.tile_keys.assign(ntile, 0);
+    P.tile_src.assign(ntile * TT, -1);
+    P.tile_cols.assign(ntile * TT, 0);
+    P.tile_cnt.assign(ntile, 0);
+    P.tile_same.assign(ntile, 0);
+    P.red_ptr.assign(T.nslots + 1, 0);
+    int64_t tl = 0;
+    for (size_t k = 0; k + 1 < kc.size(); ++k)
+      for (int64_t b = kc[k]; b < kc[k + 1]; b += TT, ++tl) {
+        const int cnt = (int)std::min<int64_t>(TT, kc[k + 1] - b);
+        P.tile_level[tl] = P.key_level[k];
+        P.tile_dir[tl] = P.key_dir[k];
+        P.tile_keys[tl] = (int32_t)k;
+        P.tile_kptr[tl + 1] = tl + 1;
+        P.tile_cnt[tl] = (uint8_t)cnt;
+        for (int c = 0; c < cnt; ++c) {
+          P.tile_tslot[tl * TT + c] = pt[b + c];
+          P.tile_src[tl * TT + c] = ps[b + c];
+          P.tile_cols[tl * TT + c] = (uint8_t)c;
+          ++P.red_ptr[pt[b + c] + 1];
+        }
+      }
+    // per target slot its pair indices (tile * TT + column), increasing (= key order)
+    for (int64_t t = 0; t < T.nslots; ++t) P.red_ptr[t + 1] += P.red_ptr[t];
+    P.red_idx.assign(np, 0);
+    {
+      std::vector<int64_t> cur(P.red_ptr.begin(), P.red_ptr.end() - 1);
+      for (int64_t t2 = 0; t2 < ntile; ++t2)
+        for (int c = 0; c < P.tile_cnt[t2]; ++c) P.red_idx[cur[P.tile_tslot[t2 * TT + c]]++] = t2 * TT + c;
+    }
+    P.item_tile.resize(ntile);
+    P.item_seq.assign(ntile, 0);
+    P.item_k0.resize(ntile);
+    P.item_k1.resize(ntile);
+    P.tile_nitem.assign(ntile, 1);
+    for (int64_t i = 0; i < ntile; ++i) {
+      P.item_tile[i] = (int32_t)i;
+      P.item_k0[i] = i;
+      P.item_k1[i] = i + 1;
+    }
+    P.m2l_pair = true;
+    P.m2l_chunk = 1;
+    P.m2l_units_exec = 0;
+    for (int64_t t = 0; t < T.nslots; ++t)
+      if (ptr[t + 1] == ptr[t]) P.m2l_zero_slots.push_back((int32_t)t);
+    MTICK("pair plan");
+    return;
   }
   std::vector<int64_t> tile_first;  // index into ts
   for (size_t i = 0; i < ts.size();) {

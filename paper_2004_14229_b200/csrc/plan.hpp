@@ -123,6 +123,11 @@ struct Plan {
   std::vector<int64_t> item_k0, item_k1;
   std::vector<int32_t> tile_nitem;
   int64_t m2l_chunk = 0;
+  // pair mode (int8 M2L, clustered sources): one key per tile, columns = (target,
+  // source) pairs; per target slot the pair indices (tile * tile + column) in key order
+  bool m2l_pair = false;
+  std::vector<int64_t> red_ptr;
+  std::vector<int64_t> red_idx;
   // target slots without any M2L contribution (to be zeroed)
   std::vector<int32_t> m2l_zero_slots;
   // rank ownership of targets (all by default)

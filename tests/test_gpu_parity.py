@@ -442,3 +442,32 @@ def test_cached_near_field():
     with pytest.raises(F.FdhError) as e:
         ops.set_cache(True)  # coincident points without the zero diagonal: singular
     assert e.value.code == F.ERR_DOMAIN
+
+
+@pytest.mark.parametrize("m", [4, 5, 6])
+def test_m2l_pair_mode(m, monkeypatch):
+    """int8 M2L in pair mode (key-major over (target, source) pairs, chosen by the
+    planner for clustered sources): against the target-tile mode and the oracle;
+    many output segments (FDH_PAIR_OUT_MB) and per-apply W digits in segments give
+    the same bits."""
+    c = CONFIGS[5]
+    tg, sr, q = make_inputs(c, nt=30000 if m < 6 else 12000, ns=15000 if m < 6 else 8000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    monkeypatch.setenv("FDH_M2L_PAIR", "0")
+    yt = F.DirectionalOperator(*args).apply(q)
+    monkeypatch.setenv("FDH_M2L_PAIR", "1")
+    op = F.DirectionalOperator(*args)
+    st = op.stats()
+    assert st["m2l_pair_mode"] == 1 and st["n_c"] > 0
+    y = op.apply(q)
+    yo = oracle.Oracle(*args).apply(q)
+    e1, e2 = oracle.rel_l2(y, yo), oracle.rel_l2(y, yt)
+    print(f"m={m}: pair mode vs oracle {e1:.2e}, vs tile mode {e2:.2e}")
+    assert e1 <= TOL and e2 <= 1e-13
+    assert np.array_equal(op.apply(q), y)  # deterministic
+    monkeypatch.setenv("FDH_PAIR_OUT_MB", "8")
+    monkeypatch.setenv("FDH_W_ONTHEFLY", "1")
+    monkeypatch.setenv("FDH_W_SLOT_MB", "64")
+    op2 = F.DirectionalOperator(*args)
+    assert op2.stats()["w_segments"] >= 3
+    assert np.array_equal(op2.apply(q), y)
