@@ -691,10 +691,11 @@ __global__ void __launch_bounds__(256) k_m2l_reduce(const int64_t* __restrict__ 
   if (c0 >= c1 || red_idx[c0] >= p1) return;
   int64_t ce = c0;  // the slot's pairs in this segment: [c0, ce)
   while (ce < c1 && red_idx[ce] < p1) ++ce;
+  // a running sum continued across segments: the same rounding whatever the segment cuts
   for (int r = threadIdx.x; r < 2 * n_pad; r += blockDim.x) {
-    double a = 0.0;
+    double a = loc[t * 2 * n_pad + r];
     for (int64_t c = c0; c < ce; ++c) a += out[(red_idx[c] - p0) * 2 * n_pad + r];
-    loc[t * 2 * n_pad + r] += a;
+    loc[t * 2 * n_pad + r] = a;
   }
   if (threadIdx.x == 0) cursor[t] = ce;
 }
