@@ -126,7 +126,8 @@ struct fdh_op {
   struct Seg {
     int item0, item1;
     int64_t key0, key1;
-    bool gen = true;  // generate the segment's W digits (on-the-fly mode; pair-mode sub-segments share them)
+    bool gen = true;   // generate the segment's W digits (on-the-fly mode; sub-segments share them)
+    bool pair = false;  // items of the pair part (int8 pair / hybrid mode)
   };
   // int8 pair mode (P.m2l_pair): per-pair output buffer of one segment, the per-slot
   // pair lists and their cursors
@@ -474,19 +475,29 @@ void setup_device(fdh_op* o) {
       CK(cudaMemsetAsync(o->Wq, 0, (size_t)(2 * slot_keys * wkq), o->st));  // padding rows / K stay zero
     }
     if (P.m2l_pair) {
-      // pair mode: segments of at most pair_cap pairs (the output buffer), cut inside
-      // the W segments when the digits are generated per apply
+      // pair part (pair / hybrid mode): segments cut at the first pair item and
+      // into at most cap_items items (the pair output buffer), inside the W
+      // segments when the digits are generated per apply
       CK(cudaMemGetInfo(&fre, &tot));
       double cap_bytes = std::min(8.0e9, 0.25 * (double)fre);
       if (const char* pb = std::getenv("FDH_PAIR_OUT_MB")) cap_bytes = std::max(1.0, std::atof(pb)) * 1048576.0;
       const int64_t TT = P.prm.tile;
       const int64_t cap_items = std::max<int64_t>(1, (int64_t)(cap_bytes / (16.0 * P.n_pad * TT)));
+      const int ip0 = (int)P.m2l_pair_item0;
       std::vector<fdh_op::Seg> base = o->segs;
-      if (base.empty()) base.push_back({0, (int)P.item_tile.size(), 0, nkeys, true});
+      if (base.empty()) base.push_back({0, (int)P.item_tile.size(), 0, nkeys, true, false});
       o->segs.clear();
-      for (const fdh_op::Seg& b : base)
-        for (int i = b.item0; i < b.item1; i += (int)cap_items)
-          o->segs.push_back({i, (int)std::min<int64_t>(b.item1, i + cap_items), b.key0, b.key1, i == b.item0});
+      for (const fdh_op::Seg& b : base) {
+        bool first = true;
+        if (b.item0 < ip0) {  // target-tile items of this W segment
+          o->segs.push_back({b.item0, std::min(b.item1, ip0), b.key0, b.key1, first, false});
+          first = false;
+        }
+        for (int i = std::max(b.item0, ip0); i < b.item1; i += (int)cap_items) {
+          o->segs.push_back({i, (int)std::min<int64_t>(b.item1, i + cap_items), b.key0, b.key1, first, true});
+          first = false;
+        }
+      }
       o->pair_out = o->alloc<double>((size_t)(cap_items * TT * 2 * P.n_pad));
       o->red_ptr = o->up(P.red_ptr);
       o->red_idx = o->up(P.red_idx);
@@ -647,11 +658,19 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.counter = o->counter;
     const int ng = npass;
     rec(o, FDH_NPHASES + 1, st);
-    if (P.m2l_pair) {
-      // pair mode: per segment the key-major M2L into the pair buffer, then the
-      // per-slot reduction into the locals (pair order = key order)
-      CK(cudaMemcpyAsync(o->red_cur, o->red_ptr, sizeof(int64_t) * (size_t)P.T.nslots, cudaMemcpyDeviceToDevice, st));
+    if (o->w_resident && o->segs.empty()) {
+      if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
+      L += 2 + ng;
+    } else {
+      // segments: W digits generated per apply into a 2-slot ring (when not
+      // resident) and / or the pair part (pair / hybrid mode): per segment the
+      // key-major M2L into the pair buffer, then the per-slot reduction into the
+      // locals (a running sum in pair order = key order)
+      if (P.m2l_pair)
+        CK(cudaMemcpyAsync(o->red_cur, o->red_ptr, sizeof(int64_t) * (size_t)P.T.nslots, cudaMemcpyDeviceToDevice,
+                           st));
       const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
+      const int64_t ip0 = P.m2l_pair_item0;
       int wslot = -1;
       for (size_t sg = 0; sg < o->segs.size(); ++sg) {
         const auto& S = o->segs[sg];
@@ -659,9 +678,8 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
         b.item0 = S.item0;
         b.n_item = S.item1 - S.item0;
         b.counter = o->counter + sg * npass;
-        b.pair_out = o->pair_out;
         if (!o->w_resident) {
-          if (S.gen) {
+          if (S.gen || wslot < 0) {
             wslot = (wslot + 1) & 1;
             launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
                                o->lvmax_w, o->Wq + (int64_t)wslot * o->w_slot_keys * wkq, n, o->nkq,
@@ -671,32 +689,16 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
           b.Wq = o->Wq + (int64_t)wslot * o->w_slot_keys * wkq;
           b.key_base = S.key0;
         }
+        if (S.pair) b.pair_out = o->pair_out;
         if (launch_m2l_i8(st, n, P.prm.tile, b) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
-        launch_m2l_reduce(st, P.T.nslots, o->red_ptr, o->red_idx, o->red_cur, o->pair_out,
-                          (int64_t)S.item0 * P.prm.tile, (int64_t)S.item1 * P.prm.tile, o->loc, np);
-        L += ng + 1;
+        L += ng;
+        if (S.pair) {
+          launch_m2l_reduce(st, P.T.nslots, o->red_ptr, o->red_idx, o->red_cur, o->pair_out,
+                            (S.item0 - ip0) * (int64_t)P.prm.tile, (S.item1 - ip0) * (int64_t)P.prm.tile, o->loc, np);
+          L += 1;
+        }
       }
       L += 3;
-    } else if (o->w_resident) {
-      if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
-      L += 2 + ng;
-    } else {
-      const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
-      for (size_t sg = 0; sg < o->segs.size(); ++sg) {
-        const auto& S = o->segs[sg];
-        int8_t* slot = o->Wq + (int64_t)(sg & 1) * o->w_slot_keys * wkq;
-        launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
-                           o->lvmax_w, slot, n, o->nkq, m2l_i8_wgroup(n, P.prm.tile), S.key0);
-        M2LI8Args b = a;
-        b.item0 = S.item0;
-        b.n_item = S.item1 - S.item0;
-        b.Wq = slot;
-        b.key_base = S.key0;
-        b.counter = o->counter + sg * npass;
-        if (launch_m2l_i8(st, n, P.prm.tile, b) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
-        L += 1 + ng;
-      }
-      L += 2;
     }
     rec(o, FDH_NPHASES + 2, st);
   } else if (o->n_item > 0) {

@@ -473,6 +473,75 @@ void build_worklists(Plan& P) {
   }
 }
 
+// Pair part of the int8 M2L plan (key-major; SURVEY.md 7 "key-major" alternative):
+// the (key, target slot, source slot) triples sorted by key, then target slot,
+// cut into tiles of TT pairs of one key, one work item per tile (one key: no
+// chain), APPENDED to the plan's tiles and items.  The kernel writes each pair's
+// n values to an output buffer; k_m2l_reduce adds them to the target slot's
+// locals as a running sum in pair order (= key order): deterministic.
+// red_ptr / red_idx: per target slot its pair indices (relative to the first
+// pair tile: (tile - pair_tile0) * TT + column), increasing.
+void append_pair_part(Plan& P, std::vector<std::array<int32_t, 3>>& kts, int TT) {
+  std::sort(kts.begin(), kts.end());
+  const int64_t np = (int64_t)kts.size();
+  const int64_t tile0 = (int64_t)P.tile_level.size(), item0 = (int64_t)P.item_tile.size();
+  P.m2l_pair_tile0 = tile0;
+  P.m2l_pair_item0 = item0;
+  int64_t ntile = 0;
+  for (int64_t b = 0; b < np;) {
+    int64_t e = b;
+    while (e < np && kts[e][0] == kts[b][0]) ++e;
+    ntile += (e - b + TT - 1) / TT;
+    b = e;
+  }
+  const int64_t nt = tile0 + ntile;
+  P.tile_level.resize(nt, 0);
+  P.tile_dir.resize(nt, 0);
+  P.tile_tslot.resize(nt * TT, -1);
+  P.tile_nitem.resize(nt, 1);
+  const int64_t kbase = (int64_t)P.tile_keys.size();
+  P.tile_keys.resize(kbase + ntile, 0);
+  P.tile_src.resize((kbase + ntile) * TT, -1);
+  P.tile_cols.resize((kbase + ntile) * TT, 0);
+  P.tile_cnt.resize(kbase + ntile, 0);
+  P.tile_same.resize(kbase + ntile, 0);
+  P.tile_kptr.resize(nt + 1, P.tile_kptr.empty() ? 0 : P.tile_kptr.back());
+  P.red_ptr.assign(P.T.nslots + 1, 0);
+  int64_t tl = tile0, kk = kbase;
+  for (int64_t b = 0; b < np;) {
+    int64_t e = b;
+    while (e < np && kts[e][0] == kts[b][0]) ++e;
+    const int32_t key = kts[b][0];
+    for (int64_t c0 = b; c0 < e; c0 += TT, ++tl, ++kk) {
+      const int cnt = (int)std::min<int64_t>(TT, e - c0);
+      P.tile_level[tl] = P.key_level[key];
+      P.tile_dir[tl] = P.key_dir[key];
+      P.tile_keys[kk] = key;
+      P.tile_kptr[tl + 1] = kk + 1;
+      P.tile_cnt[kk] = (uint8_t)cnt;
+      for (int c = 0; c < cnt; ++c) {
+        P.tile_tslot[tl * TT + c] = kts[c0 + c][1];
+        P.tile_src[kk * TT + c] = kts[c0 + c][2];
+        P.tile_cols[kk * TT + c] = (uint8_t)c;
+        ++P.red_ptr[kts[c0 + c][1] + 1];
+      }
+      P.item_tile.push_back((int32_t)tl);
+      P.item_seq.push_back(0);
+      P.item_k0.push_back(kk);
+      P.item_k1.push_back(kk + 1);
+    }
+    b = e;
+  }
+  for (int64_t t = 0; t < P.T.nslots; ++t) P.red_ptr[t + 1] += P.red_ptr[t];
+  P.red_idx.assign(np, 0);
+  std::vector<int64_t> cur(P.red_ptr.begin(), P.red_ptr.end() - 1);
+  for (int64_t t2 = tile0; t2 < nt; ++t2) {
+    const int64_t k2 = P.tile_kptr[t2];
+    for (int c = 0; c < P.tile_cnt[k2]; ++c) P.red_idx[cur[P.tile_tslot[t2 * TT + c]]++] = (t2 - tile0) * TT + c;
+  }
+  P.m2l_pair = np > 0;
+}
+
 // M2L tiles: target slots grouped by (level, direction, lattice parity) share
 // (almost) the same key list; a tile = `tile` such slots, the union of their
 // keys, and for every key the source slot of each column (-1 if none).
@@ -614,75 +683,26 @@ void build_m2l(Plan& P) {
                    (long long)k16, (long long)k32, useful, TT, pair_mode ? " (pair mode)" : "");
   }
   if (pair_mode) {
-    // ---- pair mode (key-major): the pairs (target slot, source slot) of every key,
-    // keys in id order, pairs of a key in target-slot order, cut into tiles of 32
-    // pairs; one item per tile (one key: no chains).  The kernel writes each pair's
-    // n values to an output buffer; k_m2l_reduce adds them to the locals per target
-    // slot in pair order (= key order): deterministic, no atomics.
-    std::vector<int64_t> kc(P.key_level.size() + 1, 0);
+    // ---- pair mode (key-major): every (target slot, key, source slot) triple
+    std::vector<std::array<int32_t, 3>> kts;
+    kts.reserve(npairs);
     for (int32_t t : ts)
-      for (int64_t q = ptr[t]; q < ptr[t + 1]; ++q) ++kc[sk[q] + 1];
-    for (size_t k = 0; k + 1 < kc.size(); ++k) kc[k + 1] += kc[k];
-    const int64_t np = kc.back();
-    std::vector<int32_t> pt(np), ps(np);
-    {
-      std::vector<int64_t> cur(kc.begin(), kc.end() - 1);
-      std::vector<int32_t> tss(ts.begin(), ts.end());
-      std::sort(tss.begin(), tss.end());  // target-slot order inside a key
-      for (int32_t t : tss)
-        for (int64_t q = ptr[t]; q < ptr[t + 1]; ++q) {
-          const int64_t o = cur[sk[q]]++;
-          pt[o] = t;
-          ps[o] = ss[q];
-        }
-    }
-    int64_t ntile = 0;
-    for (size_t k = 0; k + 1 < kc.size(); ++k) ntile += (kc[k + 1] - kc[k] + TT - 1) / TT;
-    P.tile_level.assign(ntile, 0);
-    P.tile_dir.assign(ntile, 0);
-    P.tile_tslot.assign(ntile * TT, -1);
-    P.tile_kptr.assign(ntile + 1, 0);
-    P.tile_keys.assign(ntile, 0);
-    P.tile_src.assign(ntile * TT, -1);
-    P.tile_cols.assign(ntile * TT, 0);
-    P.tile_cnt.assign(ntile, 0);
-    P.tile_same.assign(ntile, 0);
-    P.red_ptr.assign(T.nslots + 1, 0);
-    int64_t tl = 0;
-    for (size_t k = 0; k + 1 < kc.size(); ++k)
-      for (int64_t b = kc[k]; b < kc[k + 1]; b += TT, ++tl) {
-        const int cnt = (int)std::min<int64_t>(TT, kc[k + 1] - b);
-        P.tile_level[tl] = P.key_level[k];
-        P.tile_dir[tl] = P.key_dir[k];
-        P.tile_keys[tl] = (int32_t)k;
-        P.tile_kptr[tl + 1] = tl + 1;
-        P.tile_cnt[tl] = (uint8_t)cnt;
-        for (int c = 0; c < cnt; ++c) {
-          P.tile_tslot[tl * TT + c] = pt[b + c];
-          P.tile_src[tl * TT + c] = ps[b + c];
-          P.tile_cols[tl * TT + c] = (uint8_t)c;
-          ++P.red_ptr[pt[b + c] + 1];
-        }
-      }
-    // per target slot its pair indices (tile * TT + column), increasing (= key order)
-    for (int64_t t = 0; t < T.nslots; ++t) P.red_ptr[t + 1] += P.red_ptr[t];
-    P.red_idx.assign(np, 0);
-    {
-      std::vector<int64_t> cur(P.red_ptr.begin(), P.red_ptr.end() - 1);
-      for (int64_t t2 = 0; t2 < ntile; ++t2)
-        for (int c = 0; c < P.tile_cnt[t2]; ++c) P.red_idx[cur[P.tile_tslot[t2 * TT + c]]++] = t2 * TT + c;
-    }
-    P.item_tile.resize(ntile);
-    P.item_seq.assign(ntile, 0);
-    P.item_k0.resize(ntile);
-    P.item_k1.resize(ntile);
-    P.tile_nitem.assign(ntile, 1);
-    for (int64_t i = 0; i < ntile; ++i) {
-      P.item_tile[i] = (int32_t)i;
-      P.item_k0[i] = i;
-      P.item_k1[i] = i + 1;
-    }
-    P.m2l_pair = true;
+      for (int64_t q = ptr[t]; q < ptr[t + 1]; ++q) kts.push_back({sk[q], t, ss[q]});
+    P.tile_level.clear();
+    P.tile_dir.clear();
+    P.tile_tslot.clear();
+    P.tile_kptr.assign(1, 0);
+    P.tile_keys.clear();
+    P.tile_src.clear();
+    P.tile_cols.clear();
+    P.tile_cnt.clear();
+    P.tile_same.clear();
+    P.item_tile.clear();
+    P.item_seq.clear();
+    P.item_k0.clear();
+    P.item_k1.clear();
+    P.tile_nitem.clear();
+    append_pair_part(P, kts, TT);
     P.m2l_chunk = 1;
     P.m2l_units_exec = 0;
     for (int64_t t = 0; t < T.nslots; ++t)
@@ -809,6 +829,63 @@ void build_m2l(Plan& P) {
     std::fprintf(stderr, "\n");
   }
   MTICK("compaction");
+  // Hybrid (int8, one rhs): (tile, key) with every valid column present stay in
+  // the target tiles; the pairs of the partial ones go to the key-major pair part
+  // (appended below) -- no absent column is issued in either part.  Chosen when
+  // the issued columns shrink by more than the pair part's lower measured rate
+  // (pair tiles ~0.6x the target tiles' issued rate, profiles/r02_m2l_pair_mode.jsonl).
+  std::vector<std::array<int32_t, 3>> hyb;
+  if (P.prm.m2l_impl == 1 && R == 1) {
+    std::vector<int32_t> nvalid(ntile, 0);
+    for (int64_t tl = 0; tl < ntile; ++tl)
+      for (int c = 0; c < TT; ++c) nvalid[tl] += P.tile_tslot[tl * TT + c] >= 0;
+    int64_t full_tk = 0, part_pairs = 0;
+    for (int64_t tl = 0; tl < ntile; ++tl)
+      for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
+        if (P.tile_cnt[i] == nvalid[tl]) ++full_tk;
+        else part_pairs += P.tile_cnt[i];
+      }
+    const double c_tile = (double)tot * TT, c_hyb = (double)full_tk * TT + (double)part_pairs / 0.6;
+    const char* hm = std::getenv("FDH_M2L_HYBRID");  // 1: force, 0: never
+    const bool hybrid = part_pairs > 0 && (hm ? hm[0] == '1' : c_hyb < 0.95 * c_tile);
+    if (mdbg)
+      std::fprintf(stderr, "[m2l] hybrid: full tile-keys %lld of %lld, partial pairs %lld, cost %.3g vs %.3g -> %s\n",
+                   (long long)full_tk, (long long)tot, (long long)part_pairs, c_hyb, c_tile, hybrid ? "yes" : "no");
+    if (hybrid) {
+      hyb.reserve(part_pairs);
+      std::vector<int64_t> nk(ntile + 1, 0);
+      for (int64_t tl = 0; tl < ntile; ++tl) {
+        for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
+          if (P.tile_cnt[i] == nvalid[tl]) {
+            ++nk[tl + 1];
+            continue;
+          }
+          for (int j = 0; j < P.tile_cnt[i]; ++j)
+            hyb.push_back({P.tile_keys[i], P.tile_tslot[tl * TT + P.tile_cols[i * TT + j]], P.tile_src[i * TT + j]});
+        }
+      }
+      for (int64_t tl = 0; tl < ntile; ++tl) nk[tl + 1] += nk[tl];
+      int64_t w = 0;  // compact the kept (tile, key) rows in place (order preserved)
+      for (int64_t tl = 0; tl < ntile; ++tl)
+        for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
+          if (P.tile_cnt[i] != nvalid[tl]) continue;
+          if (w != i) {
+            P.tile_keys[w] = P.tile_keys[i];
+            P.tile_cnt[w] = P.tile_cnt[i];
+            P.tile_same[w] = P.tile_same[i];
+            std::copy(P.tile_src.begin() + i * TT, P.tile_src.begin() + (i + 1) * TT, P.tile_src.begin() + w * TT);
+            std::copy(P.tile_cols.begin() + i * TT, P.tile_cols.begin() + (i + 1) * TT, P.tile_cols.begin() + w * TT);
+          }
+          ++w;
+        }
+      P.tile_kptr.assign(nk.begin(), nk.end());
+      P.tile_keys.resize(w);
+      P.tile_cnt.resize(w);
+      P.tile_same.resize(w);
+      P.tile_src.resize(w * TT);
+      P.tile_cols.resize(w * TT);
+    }
+  }
   // Work items = (tile, global key chunk), launched chunk-major: the CTAs in
   // flight at any moment all work inside ~one chunk of key ids, so each
   // coupling matrix is read from HBM about once and then served from L2 to
@@ -896,6 +973,10 @@ void build_m2l(Plan& P) {
       for (int64_t j = P.item_k0[i]; j < P.item_k1[i]; ++j) flushes += (j == P.item_k0[i] || !P.tile_same[j]);
     std::fprintf(stderr, "[m2l] items %lld  column-map runs %lld (%.2f keys per run)\n", (long long)P.item_k0.size(),
                  (long long)flushes, (double)tot / (double)std::max<int64_t>(1, flushes));
+  }
+  if (!hyb.empty()) {
+    append_pair_part(P, hyb, TT);
+    MTICK("hybrid pairs");
   }
   // target slots with no M2L contribution
   for (int64_t t = 0; t < T.nslots; ++t)

@@ -126,6 +126,7 @@ struct Plan {
   // pair mode (int8 M2L, clustered sources): one key per tile, columns = (target,
   // source) pairs; per target slot the pair indices (tile * tile + column) in key order
   bool m2l_pair = false;
+  int64_t m2l_pair_tile0 = 0, m2l_pair_item0 = 0;  // first pair tile / item (hybrid: after the target tiles)
   std::vector<int64_t> red_ptr;
   std::vector<int64_t> red_idx;
   // target slots without any M2L contribution (to be zeroed)

@@ -471,3 +471,30 @@ def test_m2l_pair_mode(m, monkeypatch):
     op2 = F.DirectionalOperator(*args)
     assert op2.stats()["w_segments"] >= 3
     assert np.array_equal(op2.apply(q), y)
+
+
+@pytest.mark.parametrize("m", [4, 6])
+def test_m2l_hybrid_mode(m, monkeypatch):
+    """int8 M2L hybrid: (tile, key) rows with every column present stay in the
+    target tiles, the pairs of the partial ones run key-major (pair part) -- the
+    same y as the plain target tiles (to FP64 summation order) and the oracle; W
+    digits generated per apply and a small pair buffer give the same bits."""
+    c = CONFIGS[2]
+    tg, sr, q = make_inputs(c, nt=30000 if m == 4 else 12000, ns=25000 if m == 4 else 10000)
+    args = (tg, sr, c.root_lo, c.root_hi, c.kappa, 32, m, c.eta2, c.l_hf)
+    monkeypatch.setenv("FDH_M2L_HYBRID", "0")
+    yt = F.DirectionalOperator(*args).apply(q)
+    monkeypatch.setenv("FDH_M2L_HYBRID", "1")
+    op = F.DirectionalOperator(*args)
+    assert op.stats()["m2l_pair_mode"] == 1
+    y = op.apply(q)
+    yo = oracle.Oracle(*args).apply(q)
+    e1, e2 = oracle.rel_l2(y, yo), oracle.rel_l2(y, yt)
+    print(f"m={m}: hybrid vs oracle {e1:.2e}, vs target tiles {e2:.2e}")
+    assert e1 <= TOL and e2 <= 1e-13
+    monkeypatch.setenv("FDH_PAIR_OUT_MB", "4")
+    monkeypatch.setenv("FDH_W_ONTHEFLY", "1")
+    monkeypatch.setenv("FDH_W_SLOT_MB", "64")
+    op2 = F.DirectionalOperator(*args)
+    assert op2.stats()["w_segments"] >= 3
+    assert np.array_equal(op2.apply(q), y)
