@@ -393,8 +393,10 @@ void setup_device(fdh_op* o) {
   const int64_t R = o->R = P.prm.nrhs;
   o->mom = o->alloc<double>((size_t)(R * P.S.nslots * np2));  // [rhs][slot][Re | Im]
   o->loc = o->alloc<double>((size_t)(R * P.T.nslots * np2));
-  if (!P.m2l_pair)  // chained tile accumulators (pair mode: one key per item, no chains)
-    o->tile_acc = o->alloc<double>((size_t)((int64_t)o->n_tile * P.n_pad * 2 * P.prm.tile));
+  {  // chained tile accumulators of the target tiles (the pair part's tiles have one item: no chain)
+    const int64_t nacc = P.m2l_pair ? P.m2l_pair_tile0 : (int64_t)o->n_tile;
+    o->tile_acc = o->alloc<double>((size_t)std::max<int64_t>(1, nacc * P.n_pad * 2 * P.prm.tile));
+  }
   o->ticket = o->alloc<int>((size_t)std::max(
       (P.prm.m2l_impl == 1 ? m2l_i8_passes(P.n, P.prm.tile) : 1) * o->n_tile, 1));  // one chain per M-block pass
   o->q = o->alloc<double2>((size_t)(R * o->ns));
