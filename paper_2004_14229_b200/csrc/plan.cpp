@@ -832,8 +832,7 @@ void build_m2l(Plan& P) {
   // Hybrid (int8, one rhs): (tile, key) with every valid column present stay in
   // the target tiles; the pairs of the partial ones go to the key-major pair part
   // (appended below) -- no absent column is issued in either part.  Chosen when
-  // the issued columns shrink by more than the pair part's lower measured rate
-  // (pair tiles ~0.6x the target tiles' issued rate, profiles/r02_m2l_pair_mode.jsonl).
+  // the issued columns shrink by more than the pair part's lower rate costs.
   std::vector<std::array<int32_t, 3>> hyb;
   if (P.prm.m2l_impl == 1 && R == 1) {
     std::vector<int32_t> nvalid(ntile, 0);
@@ -845,7 +844,11 @@ void build_m2l(Plan& P) {
         if (P.tile_cnt[i] == nvalid[tl]) ++full_tk;
         else part_pairs += P.tile_cnt[i];
       }
-    const double c_tile = (double)tot * TT, c_hyb = (double)full_tk * TT + (double)part_pairs / 0.6;
+    // pair-part rate relative to the target tiles: the per-item epilogue and
+    // pipeline refill cost ~10 stages of K per item of nch stages (measured:
+    // m = 4 0.44, m = 5 0.58, m = 6 0.69 -- profiles/r02_m2l_pair_mode.jsonl, _hybrid.jsonl)
+    const double nch = 2.0 * ((P.n + 15) / 16 * 16) / 32.0, rate = nch / (nch + 10.0);
+    const double c_tile = (double)tot * TT, c_hyb = (double)full_tk * TT + (double)part_pairs / rate;
     const char* hm = std::getenv("FDH_M2L_HYBRID");  // 1: force, 0: never
     const bool hybrid = part_pairs > 0 && (hm ? hm[0] == '1' : c_hyb < 0.95 * c_tile);
     if (mdbg)
