@@ -154,6 +154,9 @@ __device__ __forceinline__ void to_digits(double x, int ex, int8_t (&d)[KS]) {
   }
   d[0] = (int8_t)X;
 }
+__device__ __forceinline__ int tile_nit_guard(const int32_t* __restrict__ tile_nitem, int tile) {
+  return tile_nitem[tile];
+}
 __device__ __forceinline__ int level_exp(const unsigned long long* lvmax, int l) {
   int ex = 0;
   frexp(__longlong_as_double((long long)lvmax[l]), &ex);
@@ -587,6 +590,367 @@ __global__ void __maxnreg__(128)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- M2L, pipelined
+// The same work items, digits and arithmetic as k_m2l_i8, with the roles fully
+// decoupled by mbarriers so that item boundaries do not drain the pipeline:
+//   warp 0      claims items in order (atomic counter), publishes {item} in a
+//               2-deep ring (meta_full / meta_empty) and streams W (cp.async.bulk);
+//   warp 1      issues the MMAs; before the first MMA of an item it waits until the
+//               epilogue warps have read the previous item's TMEM (tfree), after the
+//               last it commits tmem_full;
+//   warps 2..   gather the moment digits; the source slot of each target column
+//   2+NGW-1     is rebuilt per key in registers from the compacted (tile, key) row
+//               (warp shuffles), prefetched one key ahead;
+//   4 warps     epilogue (TMEM -> FP64 -> chained tile accumulator / locals / pair
+//               buffer), the ticket chain as before; its TMEM read overlaps the
+//               next item's W / moment loads.
+// Forward progress: as k_m2l_i8 (items claimed in increasing order by running CTAs).
+template <int MB, int TT, int KS, int NST, int NGW>
+__global__ void __maxnreg__(128)
+    k_m2l_i8p(const int32_t* __restrict__ item_tile, const int32_t* __restrict__ item_seq,
+              const int64_t* __restrict__ item_k0, const int64_t* __restrict__ item_k1,
+              const int32_t* __restrict__ tile_nitem, const int32_t* __restrict__ tile_tslot,
+              const int32_t* __restrict__ tile_level, const int32_t* __restrict__ tile_keys,
+              const int32_t* __restrict__ tile_src, const uint8_t* __restrict__ tile_cols,
+              const uint8_t* __restrict__ tile_cnt, const int8_t* __restrict__ Wq, const int8_t* __restrict__ Mq,
+              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
+              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
+              int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int mb_tot, int blk0,
+              int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out) {
+  using S = I8Shape<MB, TT, KS, NST, NGW>;
+  constexpr int NC = S::NC;
+  constexpr int EW0 = 2 + NGW;  // first epilogue warp
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* wst = smem;
+  uint8_t* bst = smem + NST * S::WST;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bst + NST * S::BST);
+  uint64_t* fullb = full + NST;
+  uint64_t* empty = fullb + NST;
+  uint64_t* meta_full = empty + NST;   // [2]
+  uint64_t* meta_empty = meta_full + 2;  // [2]: NGW gather + 1 MMA + 4 epilogue warps
+  uint64_t* tmem_full = meta_empty + 2;
+  uint64_t* tfree = tmem_full + 1;
+  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tfree + 1);
+  __shared__ int s_idx[2];
+  __shared__ double csc[TT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kp = 2 * nkq, nch = kp / kKC;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(fullb + s, NGW);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(meta_full + b, 1);
+      mbar_init(meta_empty + b, NGW + 1 + 4);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tfree, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tbase_s;
+
+  if (warp == 0) {
+    // ---------------- producer: claims + W stream
+    uint32_t qbase = 0;
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait_sleep(meta_empty + b, ((it - 2) >> 1) & 1);
+      int idx = 0;
+      if (lane == 0) {
+        idx = atomicAdd(counter, 1);
+        s_idx[b] = idx;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_full + b)) : "memory");
+      }
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= n_item) break;
+      const int item = item0 + idx;
+      const int64_t k0 = item_k0[item], k1 = item_k1[item];
+      const int Q = (int)(k1 - k0) * nch;
+      int kq = 0, ch = 0;
+      int key = tile_keys[k0];
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
+        if (lane == 0) {
+          mbar_expect_tx(full + s, S::WST);
+          bulk_g2s(wst + s * S::WST,
+                   Wq + (((int64_t)key - key_base) * nch + ch) * (KS * mb_tot * kCore) + blk0 * (KS * kCore), S::WST,
+                   full + s);
+        }
+        __syncwarp();
+        if (++ch == nch) {
+          ch = 0;
+          ++kq;
+          if (k0 + kq < k1) key = tile_keys[k0 + kq];
+        }
+      }
+      qbase += (uint32_t)Q;
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    const uint64_t dA0 = sdesc(smem_u32(wst)), dB0 = sdesc(smem_u32(bst));
+    uint32_t qbase = 0;
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      mbar_wait(meta_full + b, (it >> 1) & 1);
+      const int idx = s_idx[b];
+      if (idx >= n_item) break;
+      const int item = item0 + idx;
+      const int Q = (int)(item_k1[item] - item_k0[item]) * nch;
+      if (it >= 1) mbar_wait(tfree, (it - 1) & 1);  // the epilogue has read the previous item's TMEM
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        const uint32_t ph = (qg / NST) & 1;
+        mbar_wait(full + s, ph);
+        mbar_wait(fullb + s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
+          const uint32_t acc0 = q > 0 ? 1u : 0u;
+#pragma unroll
+          for (int i = 0; i < KS; ++i) {
+            const int ncol = (S::LV - i) * NC;
+#pragma unroll
+            for (int bb = 0; bb < MB; ++bb) {
+              const int nsp = (ncol + 255) / 256;
+              const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
+#pragma unroll
+              for (int p0 = 0; p0 < ncol;) {
+                const int np = ncol - p0 < part ? ncol - p0 : part;
+                mma_i8(tmem + bb * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + bb) * kCore) >> 4),
+                       dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
+                p0 += np;
+              }
+            }
+          }
+          mma_commit(empty + s);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        mma_commit(tmem_full);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
+      }
+      __syncwarp();
+      qbase += (uint32_t)Q;
+    }
+  } else if (warp < EW0) {
+    // ---------------- gather
+    constexpr int RND = (KS * 4 + 7) / 8;
+    constexpr int U = (TT / 4) * RND;
+    constexpr int UPW = (U + NGW - 1) / NGW;
+    constexpr int G = 1;
+    int dsto[UPW], gofs[UPW], ccol[UPW];
+    {
+      const int cl = lane >> 3, p8 = lane & 7;
+#pragma unroll
+      for (int t = 0; t < UPW; ++t) {
+        const int u = (warp - 2) + t * NGW;
+        const int cg = u / RND, r = u % RND;
+        const int pc = 8 * r + p8;
+        const int c = 4 * cg + cl;
+        const bool ok = u < U && pc < KS * 4;
+        const int h = pc & 1, kb = (pc >> 1) & 1, j = pc >> 2;
+        const int n = j * NC + 2 * c + h;
+        dsto[t] = ok ? ((n >> 3) * 2 + kb) * 128 + (n & 7) * 16 : -1;
+        gofs[t] = pc * 16;
+        ccol[t] = ok ? c : 0;
+      }
+    }
+    auto arrive = [&](uint32_t qa) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
+    };
+    // source slot of column `lane` of the compacted (tile, key) row kk (-1: absent)
+    auto row_src = [&](int64_t kk, int& col, int& src) {
+      const int cnt = tile_cnt[kk];
+      col = lane < cnt ? (int)tile_cols[kk * TT + lane] : -1;
+      src = lane < cnt ? tile_src[kk * TT + lane] : -1;
+    };
+    auto expand = [&](int col, int src) {  // lane = column -> its source slot
+      int mine = -1;
+#pragma unroll 4
+      for (int j = 0; j < TT; ++j) {
+        const int cj = __shfl_sync(0xffffffffu, col, j), sj = __shfl_sync(0xffffffffu, src, j);
+        if (cj == lane) mine = sj;
+      }
+      return mine;
+    };
+    uint32_t qbase = 0;
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      mbar_wait_sleep(meta_full + b, (it >> 1) & 1);
+      const int idx = s_idx[b];
+      if (idx >= n_item) break;
+      const int item = item0 + idx;
+      const int64_t k0 = item_k0[item], k1 = item_k1[item];
+      const int Q = (int)(k1 - k0) * nch;
+      int ncol, nsrc;
+      row_src(k0, ncol, nsrc);
+      int srcl = expand(ncol, nsrc);
+      if (k0 + 1 < k1) row_src(k0 + 1, ncol, nsrc);  // prefetch the next key's row
+      int srcv[UPW];
+#pragma unroll
+      for (int t = 0; t < UPW; ++t) srcv[t] = __shfl_sync(0xffffffffu, srcl, ccol[t]);
+      int kq = 0, ch = 0;
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t qg = qbase + q;
+        const int s = qg % NST;
+        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
+        uint8_t* bb = bst + s * S::BST;
+        const int8_t* mq = Mq + (int64_t)ch * (KS * 64);
+#pragma unroll
+        for (int t = 0; t < UPW; ++t) {
+          if (dsto[t] < 0) continue;
+          if (srcv[t] >= 0) cp_async16(bb + dsto[t], mq + (int64_t)srcv[t] * nch * (KS * 64) + gofs[t]);
+          else *reinterpret_cast<int4*>(bb + dsto[t]) = make_int4(0, 0, 0, 0);
+        }
+        cp_async_commit();
+        if (q >= G) {
+          cp_async_wait<G>();
+          arrive(qg - G);
+        }
+        if (++ch == nch) {
+          ch = 0;
+          ++kq;
+          if (k0 + kq < k1) {
+            srcl = expand(ncol, nsrc);
+            if (k0 + kq + 1 < k1) row_src(k0 + kq + 1, ncol, nsrc);
+#pragma unroll
+            for (int t = 0; t < UPW; ++t) srcv[t] = __shfl_sync(0xffffffffu, srcl, ccol[t]);
+          }
+        }
+      }
+      cp_async_wait<0>();
+      for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qbase + qa);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
+      qbase += (uint32_t)Q;
+    }
+  } else {
+    // ---------------- epilogue (4 warps, TMEM lane quarter = warp & 3)
+    const int qw = warp & 3;
+    double fL[S::LV];
+#pragma unroll
+    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
+    for (int it = 0;; ++it) {
+      const int b = it & 1;
+      mbar_wait_sleep(meta_full + b, (it >> 1) & 1);
+      const int idx = s_idx[b];
+      if (idx >= n_item) break;
+      const int item = item0 + idx;
+      const int tile = item_tile[item];
+      const int seq = item_seq[item], nit = tile_nit_guard(tile_nitem, tile);
+      const int lvl = tile_level[tile];
+      mbar_wait_sleep(tmem_full, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // csc and the ticket wait among the 4 epilogue warps (named barrier 1)
+      if (warp == EW0 && lane < TT)
+        csc[lane] = ldexp(1.0, level_exp(lvmax_w, lvl) + 2 + level_exp(lvmax_v, (lane % nrhs) * kMaxLevels + lvl));
+      if (seq > 0 && warp == EW0 && lane == 0)
+        while (ld_acquire(ticket + tick_off + tile) != seq) __nanosleep(100);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const bool last = seq == nit - 1;
+      double* A = tile_acc + (int64_t)tile * n_pad * NC;
+#pragma unroll 1
+      for (int bb = 0; bb < MB; ++bb) {
+        const int row = (blk0 + bb) * 128 + qw * 32 + lane;
+#pragma unroll 1
+        for (int g = 0; g < NC / 8; ++g) {
+          uint32_t r[S::LV][8];
+#pragma unroll
+          for (int L = 0; L < S::LV; ++L)
+            tmem_ld8(tmem + ((uint32_t)(qw * 32) << 16) + bb * S::LV * NC + L * NC + 8 * g, r[L]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (row >= n_pad) continue;
+          double v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            double a = 0.0;
+#pragma unroll
+            for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
+            v[e] = a * csc[(8 * g + e) >> 1];
+          }
+          if (pair_out) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = 8 * g + e;
+              pair_out[((int64_t)idx * TT + (col >> 1)) * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
+            }
+            continue;
+          }
+          double* pa = A + (int64_t)row * NC + 8 * g;
+          if (seq > 0) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] += __ldcg(pa + e);
+          }
+          if (last) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = 8 * g + e;
+              const int32_t ts = tile_tslot[tile * TT + (col >> 1)];
+              if (ts >= 0) loc[(int64_t)ts * 2 * n_pad + (col & 1) * n_pad + row] = v[e];
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) __stcg(pa + e, v[e]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      if (!last) __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == EW0 && lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tfree)) : "memory");
+        if (!last) st_release(ticket + tick_off + tile, seq + 1);
+      }
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int MB, int TT, int NST, int NGW>
+size_t i8p_smem() {
+  using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
+  return (size_t)NST * S::STAGE + (3 * NST + 6) * 8 + 16;
+}
+
+template <int MB, int TT, int NST, int NGW>
+void run_i8p(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass) {
+  auto kern = k_m2l_i8p<MB, TT, kI8Digits, NST, NGW>;
+  const size_t sm = i8p_smem<MB, TT, NST, NGW>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = std::max(1, std::min(a.n_item, nsm));
+  kern<<<grid, (2 + NGW + 4) * 32, sm, st>>>(a.item_tile, a.item_seq, a.item_k0, a.item_k1, a.tile_nitem,
+                                            a.tile_tslot, a.tile_level, a.tile_keys, a.tile_src, a.tile_cols,
+                                            a.tile_cnt, a.Wq, a.Mq, a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc,
+                                            a.counter + pass, a.item0, a.n_item, a.nkq, a.n_pad, mb_tot, blk0,
+                                            pass * a.n_tile, a.key_base, a.nrhs, a.pair_out);
+}
+
 template <int MB, int TT, int NST, int NGW>
 size_t i8_smem(int fkeys) {
   using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
@@ -649,8 +1013,28 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
   const int mb = (n + 127) / 128;
+  // the pipelined kernel (k_m2l_i8p) by default; FDH_I8_PIPE=0 selects k_m2l_i8
+  static const bool pipe = [] {
+    const char* e = std::getenv("FDH_I8_PIPE");
+    return !(e && e[0] == '0');
+  }();
   // passes over the item list (m2l_i8_passes): one per M-block group; a.counter
-  // holds one zeroed claim counter per pass (and per on-the-fly segment)
+  // holds one zeroed claim counter per pass (and per segment)
+  if (pipe) {
+    if (mb == 1 && tile == 32) {
+      run_i8p<1, 32, 5, 8>(st, a, 1, 0, 0);
+    } else if (mb == 2 && tile == 16) {
+      run_i8p<2, 16, 3, 8>(st, a, 2, 0, 0);
+    } else if (mb == 3 && tile == 16) {
+      run_i8p<2, 16, 3, 8>(st, a, 3, 0, 0);
+      run_i8p<1, 16, 6, 8>(st, a, 3, 2, 1);
+    } else if (mb >= 2 && tile == 32) {
+      for (int b = 0; b < mb; ++b) run_i8p<1, 32, 5, 8>(st, a, mb, b, b);
+    } else {
+      return 1;
+    }
+    return 0;
+  }
   if (mb == 1 && tile == 32) {
     run_i8<1, 32, 4, 8, 1>(st, a, 1, 0, 0);
   } else if (mb == 2 && tile == 16) {
@@ -662,9 +1046,8 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
     run_i8<2, 16, 3, 8, 1>(st, a, 3, 0, 0);
     run_i8<1, 16, 4, 8, 1>(st, a, 3, 2, 1);
   } else if (mb >= 2 && tile == 32) {
-    // 32 target columns (N up to 448 per W digit): one 128-row M-block per pass
-    // 5 stages fit beside the m = 5, 6 item tables (fkeys <= 128): deeper W / B
-    // lookahead (FDH_I8_NST=4 selects the 4-stage ring of the m <= 4 kernel)
+    // 32 target columns (N up to 448 per W digit): one 128-row M-block per pass;
+    // 5 stages fit beside the m = 5, 6 item tables (fkeys <= 128)
     static const int nst = [] {
       const char* e = std::getenv("FDH_I8_NST");
       return e ? std::atoi(e) : 5;
@@ -679,6 +1062,7 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   }
   return 0;
 }
+
 namespace {
 // pair mode: loc[t] += sum of its pairs' outputs of this segment [p0, p1), in pair
 // order (cursor[t] advances through the slot's sorted pair list segment by segment)
