@@ -18,8 +18,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,nohe
 case "$task" in
   smoke) python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log ;;
   tests)
-    if [ $# -gt 0 ]; then timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu -k "$*" > gpurun_out/pytest_$tag.log 2>&1
-    else timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu > gpurun_out/pytest_$tag.log 2>&1; fi
+    if [ $# -gt 0 ]; then timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu --timeout=${TEST_TIMEOUT:-900} -k "$*" > gpurun_out/pytest_$tag.log 2>&1
+    else timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -q -m gpu --timeout=${TEST_TIMEOUT:-900} > gpurun_out/pytest_$tag.log 2>&1; fi
     echo "pytest rc=$?"; grep -E "passed|failed|^FAILED|^ERROR" gpurun_out/pytest_$tag.log | tail -15 ;;
   bench) timeout ${BENCH_TIMEOUT:-2400} python bench.py "$@" > gpurun_out/bench_$tag.jsonl 2> gpurun_out/bench_$tag.err
     echo "bench rc=$?"; tail -c 3000 gpurun_out/bench_$tag.jsonl; tail -5 gpurun_out/bench_$tag.err ;;
