@@ -220,6 +220,7 @@ def test_m2l_int8_item_split(monkeypatch):
     tg, sr, q = make_inputs(c, nt=40000, ns=40000)
     args = (tg, sr, c.root_lo, c.root_hi, c.kappa, c.n_max, c.m, c.eta2, c.l_hf)
     monkeypatch.setenv("FDH_M2L_HYBRID", "0")  # chained target-tile items only
+    monkeypatch.setenv("FDH_M2L_PAIR", "0")
     op = F.DirectionalOperator(*args)
     y = op.apply(q)
     monkeypatch.setenv("FDH_M2L_FKEYS", "8")
