@@ -1013,11 +1013,15 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
   const int mb = (n + 127) / 128;
-  // the pipelined kernel (k_m2l_i8p) by default; FDH_I8_PIPE=0 selects k_m2l_i8
-  static const bool pipe = [] {
+  // the pipelined kernel (k_m2l_i8p) for two or more M-blocks and for pair items
+  // (measured: config 5 pair mode 964 -> 817 ms, m = 6 hybrid 3337 -> 3176 ms) and
+  // k_m2l_i8 for one M-block target tiles (m <= 4: 29.3 vs 32.5 ms on config 2);
+  // FDH_I8_PIPE=0 / 1 forces one of them (profiles/r02_m2l_pipe_ab.log)
+  static const int pipe_env = [] {
     const char* e = std::getenv("FDH_I8_PIPE");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
+  const bool pipe = pipe_env >= 0 ? pipe_env == 1 : !(mb == 1 && a.pair_out == nullptr);
   // passes over the item list (m2l_i8_passes): one per M-block group; a.counter
   // holds one zeroed claim counter per pass (and per segment)
   if (pipe) {
