@@ -235,18 +235,20 @@ def roofline_block(st, c, m2l_flops, peak, gemm_ms, ms_per_step, traffic):
     if st["m2l_impl"] == 1:
         import paper_2004_14229_b200 as F
         tops = F.tensor_peak_tops(0)
-        # algorithmic int8 work: the 28 digit-pair products (i + j <= 6 of 7 digits) of every
-        # real MAC of the complex product (4 n^2 per block, 2 ops per MAC)
-        alg = 28.0 * m2l_flops
+        # algorithmic int8 work: the KS (KS + 1) / 2 digit-pair products (i + j <= KS - 1) of every
+        # real MAC of the complex product (4 n^2 per block, 2 ops per MAC); KS x bits from the library
+        ks, bits = int(st["m2l_i8_digits"]), int(st["m2l_i8_bits"])
+        npair = int(st["m2l_i8_products"])
+        alg = float(npair) * m2l_flops
         ach = alg / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         iss = st["m2l_i8_ops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-        return {"bound": "tensor", "kernel": "k_m2l_i8 (tcgen05.mma kind::i8, exact 7-digit fixed-point products, "
-                                            "TMEM int32 level accumulators)",
+        return {"bound": "tensor", "kernel": f"k_m2l_i8 (tcgen05.mma kind::i8, exact {ks} x {bits}-bit digit fixed-point "
+                                            f"products, TMEM int32 level accumulators)",
                 "achieved": ach, "peak": tops, "unit": "TOPS", "frac": (ach / tops) if (ach and tops) else None,
                 "traffic": traffic,
                 "peak_source": "measured live: fdh_tensor_peak_tops(0) int8 tcgen05 microbenchmark, M=128 N=256 "
                                "(MEASURED_PEAKS.json has no int8 entry; 2 x its bf16 burst for comparison)",
-                "algorithmic": f"28 digit products x 8 n^2 ops per admissible block x N_C={st['n_c']} = {alg:.4g} "
+                "algorithmic": f"{npair} digit products x 8 n^2 ops per admissible block x N_C={st['n_c']} = {alg:.4g} "
                                f"int8 ops per apply",
                 "issued_ops": st["m2l_i8_ops"], "issued_frac": (iss / tops) if (iss and tops) else None,
                 "issued_note": "int8 ops the kernel issues: every target column of a tile for every key of the tile "
@@ -382,8 +384,8 @@ def run_ours(args, c, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
-        "dtype": ("complex128 (f64; M2L as exact int8 x int8 -> int32 digit products of 49-bit fixed-point operands "
-                  "on tcgen05)" if st["m2l_impl"] == 1 else "complex128 (f64)"),
+        "dtype": (f"complex128 (f64; M2L as exact int8 x int8 -> int32 digit products of "
+                  f"{st['m2l_i8_digits'] * st['m2l_i8_bits']}-bit fixed-point operands on tcgen05)" if st["m2l_impl"] == 1 else "complex128 (f64)"),
         "data": "synthetic (seeded uniform / Gaussian-mixture points, U(-1,1) complex charges; SURVEY.md 8(d))",
         "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": f"target-leaf shards x{world}",
                    "l2": "flushed between timed steps (256 MB write, outside the step events); the apply's working "

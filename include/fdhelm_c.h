@@ -100,6 +100,9 @@ typedef struct fdh_stats {
   int64_t aca_dense_keys;       /* keys kept dense (2 k n >= n^2)                          */
   int64_t nf_cache_bytes;       /* device bytes of the cached near-field kernel values     */
   int64_t m2l_pair_mode;        /* 1: int8 M2L key-major on (target, source) pairs         */
+  int64_t m2l_i8_digits;        /* int8 M2L: digits per FP64 value ...                     */
+  int64_t m2l_i8_bits;          /* ... of this many bits                                   */
+  int64_t m2l_i8_products;      /* digit-pair products kept per real MAC (6 x 8 + level 6: 26) */
 } fdh_stats;
 
 /* Setup: both cluster trees (Alg. 1), the direction table

@@ -48,7 +48,9 @@ class FdhStats(C.Structure):
                 ("nrhs", C.c_int64), ("hbm_bytes", C.c_int64 * 4), ("graph_replays", C.c_int64),
                 ("apply_ms_sum", C.c_double), ("applies_collected", C.c_int64), ("aca_eps", C.c_double),
                 ("aca_mean_rank", C.c_double), ("aca_bytes", C.c_int64), ("aca_dense_keys", C.c_int64),
-                ("nf_cache_bytes", C.c_int64), ("m2l_pair_mode", C.c_int64)]
+                ("nf_cache_bytes", C.c_int64), ("m2l_pair_mode", C.c_int64),
+                ("m2l_i8_digits", C.c_int64), ("m2l_i8_bits", C.c_int64),
+                ("m2l_i8_products", C.c_int64)]
 
 
 class FdhError(RuntimeError):

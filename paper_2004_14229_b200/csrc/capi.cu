@@ -485,38 +485,19 @@ void setup_device(fdh_op* o) {
       if (const char* pb = std::getenv("FDH_PAIR_OUT_MB")) cap_bytes = std::max(1.0, std::atof(pb)) * 1048576.0;
       const int64_t TT = P.prm.tile;
       const int64_t cap_items = std::max<int64_t>(1, (int64_t)(cap_bytes / (16.0 * P.n_pad * TT)));
-      const int ip0 = (int)P.m2l_pair_item0, ni = (int)P.item_tile.size();
+      const int ip0 = (int)P.m2l_pair_item0;
+      std::vector<fdh_op::Seg> base = o->segs;
+      if (base.empty()) base.push_back({0, (int)P.item_tile.size(), 0, nkeys, true, false});
       o->segs.clear();
-      auto push_pairs = [&](int i0, int i1, int64_t k0, int64_t k1, bool gen) {
-        for (int i = i0; i < i1; i += (int)cap_items) {
-          o->segs.push_back({i, (int)std::min<int64_t>(i1, i + cap_items), k0, k1, gen, true});
-          gen = false;
+      for (const fdh_op::Seg& b : base) {
+        bool first = true;
+        if (b.item0 < ip0) {  // target-tile items of this W segment
+          o->segs.push_back({b.item0, std::min(b.item1, ip0), b.key0, b.key1, first, false});
+          first = false;
         }
-      };
-      if (o->w_resident) {
-        if (ip0 > 0) o->segs.push_back({0, ip0, 0, nkeys, false, false});
-        push_pairs(ip0, ni, 0, nkeys, false);
-      } else {
-        // per W slot (key range): its target-tile items, then its pair items, so the
-        // slot's digits are generated once for both parts (both are key-ordered)
-        const int64_t sk = o->w_slot_keys;
-        auto slot_of = [&](int i) { return (int64_t)P.tile_keys[P.item_k0[i]] / sk; };
-        int it = 0, ip = ip0;
-        while (it < ip0 || ip < ni) {
-          const int64_t sl = std::min(it < ip0 ? slot_of(it) : INT64_MAX, ip < ni ? slot_of(ip) : INT64_MAX);
-          const int64_t k0 = sl * sk, k1 = std::min(nkeys, (sl + 1) * sk);
-          bool gen = true;
-          int j = it;
-          while (j < ip0 && slot_of(j) == sl) ++j;
-          if (j > it) {
-            o->segs.push_back({it, j, k0, k1, true, false});
-            gen = false;
-          }
-          it = j;
-          j = ip;
-          while (j < ni && slot_of(j) == sl) ++j;
-          if (j > ip) push_pairs(ip, j, k0, k1, gen);
-          ip = j;
+        for (int i = std::max(b.item0, ip0); i < b.item1; i += (int)cap_items) {
+          o->segs.push_back({i, (int)std::min<int64_t>(b.item1, i + cap_items), b.key0, b.key1, first, true});
+          first = false;
         }
       }
       o->pair_out = o->alloc<double>((size_t)(cap_items * TT * 2 * P.n_pad));
@@ -615,12 +596,16 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     CK(cudaEventRecord(o->ev_nf, o->st2));
   }
   CK(cudaMemsetAsync(o->loc, 0, sizeof(double) * (size_t)(R * lstr), st));
-  if (o->n_item > 0 && o->aca_eps > 0.0) {
+  const bool aca = o->n_item > 0 && o->aca_eps > 0.0;
+  // ACA over a pair / hybrid plan: the low-rank M2L runs the target-tile items, the
+  // pair part (partial (tile, key) rows) stays on the exact int8 path below
+  const bool aca_pairs = aca && o->i8 && P.m2l_pair;
+  if (aca && (!P.m2l_pair || P.m2l_pair_item0 > 0)) {
     // ACA-compressed coupling (fdh_set_aca): the low-rank M2L over the same plan
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)o->n_tile, st));
     CK(cudaMemsetAsync(o->counter, 0, sizeof(int), st));
     M2LAcaArgs a;
-    a.n_item = o->n_item;
+    a.n_item = P.m2l_pair ? (int)P.m2l_pair_item0 : o->n_item;
     a.item_tile = o->item_tile;
     a.item_seq = o->item_seq;
     a.item_k0 = o->item_k0;
@@ -643,8 +628,10 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.counter = o->counter;
     rec(o, FDH_NPHASES + 1, st);
     if (launch_m2l_aca(st, n, np, P.prm.tile, a) != 0) throw PlanError{4, "ACA M2L: n > 384 not compiled"};
-    rec(o, FDH_NPHASES + 2, st);
+    if (!aca_pairs) rec(o, FDH_NPHASES + 2, st);
     L += 1;
+  }
+  if (aca && !aca_pairs) {
   } else if (o->n_item > 0 && o->i8) {
     const int npass = m2l_i8_passes(n, P.prm.tile);
     CK(cudaMemsetAsync(o->ticket, 0, sizeof(int) * (size_t)(npass * o->n_tile), st));
@@ -678,7 +665,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
     a.nrhs = R;
     a.counter = o->counter;
     const int ng = npass;
-    rec(o, FDH_NPHASES + 1, st);
+    if (!aca_pairs) rec(o, FDH_NPHASES + 1, st);
     if (o->w_resident && o->segs.empty()) {
       if (launch_m2l_i8(st, n, P.prm.tile, a) != 0) throw PlanError{4, "no int8 M2L kernel for this n / tile"};
       L += 2 + ng;
@@ -693,14 +680,17 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
       const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
       const int64_t ip0 = P.m2l_pair_item0;
       int wslot = -1;
+      int64_t wkey0 = -1;  // first key of the digits in the current W slot
       for (size_t sg = 0; sg < o->segs.size(); ++sg) {
         const auto& S = o->segs[sg];
+        if (aca_pairs && !S.pair) continue;  // target-tile items done by the ACA kernel
         M2LI8Args b = a;
         b.item0 = S.item0;
         b.n_item = S.item1 - S.item0;
         b.counter = o->counter + sg * npass;
         if (!o->w_resident) {
-          if (S.gen || wslot < 0) {
+          if (S.key0 != wkey0) {  // sub-segments of one key range share the slot's digits
+            wkey0 = S.key0;
             wslot = (wslot + 1) & 1;
             launch_coupling_i8(st, o->dC, o->dirtab, S.key0, S.key1 - S.key0, o->key_level, o->key_d, o->key_dir, 1,
                                o->lvmax_w, o->Wq + (int64_t)wslot * o->w_slot_keys * wkq, n, o->nkq,
@@ -968,6 +958,7 @@ int create_common(const double* tx, const double* ty, const double* tz, int64_t 
       prm.tile = (nbox <= 128 || nbox > 384) ? 32 : -1;
       if (const char* tt = std::getenv("FDH_I8_TILE"))  // testing knob: force 16 or 32 for m = 5, 6
         prm.tile = prm.tile > 0 ? prm.tile : (std::atoi(tt) == 32 ? 32 : 16);
+      prm.i8_digits = kI8Digits;
       prm.m2l_fkeys = m2l_i8_fkeys((nbox + 15) / 16 * 16);
       if (const char* fk = std::getenv("FDH_M2L_FKEYS"))  // testing knob: shorter items (more chaining)
         prm.m2l_fkeys = std::max(1, std::min(prm.m2l_fkeys, std::atoi(fk)));
@@ -1491,12 +1482,15 @@ int fdh_get_stats(const fdh_op* o, fdh_stats* s) {
   s->aca_bytes = o->aca_bytes;
   s->nf_cache_bytes = o->nf_bytes;
   s->m2l_pair_mode = P.m2l_pair ? 1 : 0;
+  s->m2l_i8_digits = kI8Digits;
+  s->m2l_i8_bits = kI8Bits;
+  s->m2l_i8_products = i8_products();
   s->total_cost = P.total_cost;
   s->m2l_flops_executed = P.m2l_units_exec * 16 * (int64_t)P.n_pad * (int64_t)P.n_k;  // DMMA issued (M2LSplit units)
   s->m2l_impl = P.prm.m2l_impl;
   if (P.prm.m2l_impl == 1) {
     // int8 MACs issued by k_m2l_i8: per (tile, key) and K byte: 128 rows x sum_i (KS - i) 2 TT columns per m-block
-    const int64_t cols = (int64_t)kI8Digits * (kI8Digits + 1) / 2 * 2 * P.prm.tile;
+    const int64_t cols = (int64_t)i8_products() * 2 * P.prm.tile;
     const int64_t nkq = (P.n + 15) / 16 * 16;
     s->m2l_flops_executed = 0;
     s->m2l_i8_ops = 2 * (int64_t)P.tile_keys.size() * ((P.n + 127) / 128) * 128 * (2 * nkq) * cols;

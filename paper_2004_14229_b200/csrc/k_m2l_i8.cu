@@ -145,21 +145,26 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // S = 2^(ex + 1) > 2 |x|.  Exact integer arithmetic after one rounding.
 template <int KS>
 __device__ __forceinline__ void to_digits(double x, int ex, int8_t (&d)[KS]) {
-  long long X = __double2ll_rn(ldexp(x, 7 * KS - ex - 1));
+  constexpr int B = kI8Bits, H = 1 << (B - 1);
+  long long X = __double2ll_rn(ldexp(x, B * KS - ex - 1));
 #pragma unroll
   for (int i = KS - 1; i > 0; --i) {
-    const long long r = ((X + 64) & 127) - 64;
+    const long long r = ((X + H) & (2 * H - 1)) - H;  // [-H, H-1]
     d[i] = (int8_t)r;
-    X = (X - r) >> 7;
+    X = (X - r) >> B;
   }
-  d[0] = (int8_t)X;
+  d[0] = (int8_t)X;  // |x / S| <= 0.4923 (level_exp) keeps the leading digit inside int8
 }
 __device__ __forceinline__ int tile_nit_guard(const int32_t* __restrict__ tile_nitem, int tile) {
   return tile_nitem[tile];
 }
+// exponent of the power-of-two scale S = 2^(ex + 1) of a level with maximum modulus mx.
+// 8-bit digits cover [-128, 127] b^-1 + ..., i.e. x / S in [-0.5, 0.498]: the maximum is
+// bumped by 2^-6 so that |x / S| <= 0.4923 always has digits (7-bit digits are symmetric)
 __device__ __forceinline__ int level_exp(const unsigned long long* lvmax, int l) {
   int ex = 0;
-  frexp(__longlong_as_double((long long)lvmax[l]), &ex);
+  const double mx = __longlong_as_double((long long)lvmax[l]);
+  frexp(kI8Bits == 8 ? mx * 1.015625 : mx, &ex);
   return ex;
 }
 
@@ -278,15 +283,56 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
   const int kp = 2 * nkq;
   const int nch = kp / kKC;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    int8_t dr[KS], di[KS];
+    int8_t dr[KS], di[KS], dn[KS];
     to_digits<KS>(g[k], ex, dr);
     to_digits<KS>(g[n_pad + k], ex, di);
+    to_digits<KS>(-g[n_pad + k], ex, dn);  // -Im v: its own digits (-(-128) is not an int8)
 #pragma unroll
     for (int i = 0; i < KS; ++i) {
       Mq[mq_off(s, nch, i, 0, k)] = dr[i];
-      Mq[mq_off(s, nch, i, 0, nkq + k)] = (int8_t)(-di[i]);
+      Mq[mq_off(s, nch, i, 0, nkq + k)] = dn[i];
       Mq[mq_off(s, nch, i, 1, k)] = di[i];
       Mq[mq_off(s, nch, i, 1, nkq + k)] = dr[i];
+    }
+  }
+}
+
+// The MMAs of one pipeline stage (K = 32): W digit i (M-block b) times the stacked
+// B digits j = 0 .. min(KS, LV - i) - 1, into the level blocks i .. (D column =
+// L * NC + target column); N > 256 splits into equal parts (multiples of 32).
+// `first`: the item's first stage overwrites -- every level block by the MMA of
+// the first W digit that touches it (level L by i = max(0, L - KS + 1)).
+template <int MB, int KS, int LV, int NC>
+__device__ __forceinline__ void issue_range(uint32_t tmem, uint64_t dA, uint64_t dB, int i, int b, int c0, int c1,
+                                            uint32_t acc) {
+  const int ncol = c1 - c0;
+  const int nsp = (ncol + 255) / 256;
+  const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
+#pragma unroll
+  for (int p0 = c0; p0 < c1;) {
+    const int np = c1 - p0 < part ? c1 - p0 : part;
+    mma_i8(tmem + b * LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
+           dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), acc);
+    p0 += np;
+  }
+}
+template <int MB, int KS, int LV, int NC, bool FIRST>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t dA, uint64_t dB) {
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {
+    const int nj = LV - i < KS ? LV - i : KS;  // B digits of W digit i
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+      if (!FIRST) {
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
+      } else if (i == 0) {
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 0u);
+      } else if (i + KS - 1 < LV) {  // this digit is the first to touch level i + KS - 1 (j = KS - 1)
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, (nj - 1) * NC, 1u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, (nj - 1) * NC, nj * NC, 0u);
+      } else {
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
+      }
     }
   }
 }
@@ -295,10 +341,9 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
 template <int MB, int TT, int KS, int NST, int NGW>
 struct I8Shape {
   static constexpr int THREADS = (2 + NGW) * 32;  // W producer, MMA issuer, NGW gather warps
-  static constexpr int GATHER = NGW * 32;
   static_assert(NGW == 2 || NGW >= 4, "epilogue warps must cover the 4 TMEM lane quarters");
   static constexpr int NC = 2 * TT;                 // real columns per digit block
-  static constexpr int LV = KS;                      // levels L = 0 .. KS-1 kept
+  static constexpr int LV = kI8Levels;               // levels L = i + j = 0 .. LV-1 kept
   static constexpr int TCOLS = MB * LV * NC;         // TMEM columns used
   static_assert(TCOLS <= 512, "TMEM");
   static constexpr int WST = KS * MB * kCore;        // W bytes per stage
@@ -453,24 +498,8 @@ __global__ void __maxnreg__(128)
           // operand offset below is a compile-time constant added to the stage base
           // (keeps the issuing thread at ~3 instructions per MMA)
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          const uint32_t acc0 = q > 0 ? 1u : 0u;
-#pragma unroll
-          for (int i = 0; i < KS; ++i) {
-            const int ncol = (S::LV - i) * NC;  // B digits j = 0 .. LV-1-i
-#pragma unroll
-            for (int b = 0; b < MB; ++b) {
-              // N > 256 splits into equal parts (multiples of 32 columns)
-              const int nsp = (ncol + 255) / 256;
-              const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
-#pragma unroll
-              for (int p0 = 0; p0 < ncol;) {
-                const int np = ncol - p0 < part ? ncol - p0 : part;
-                mma_i8(tmem + b * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
-                       dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
-                p0 += np;
-              }
-            }
-          }
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
           mma_commit(empty + s);
         }
         __syncwarp();
@@ -529,7 +558,7 @@ __global__ void __maxnreg__(128)
     double fL[S::LV];  // level weights 2^(-7(L+2)); the power-of-two scale S_W S_V of the
                        // column's rhs is applied after the (exact) level sum
 #pragma unroll
-    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
+    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -kI8Bits * (L + 2));
     double* A = tile_acc + (int64_t)tile * n_pad * NC;
     const int qw = warp & 3;  // TMEM lane quarter of this warp
 #pragma unroll 1
@@ -718,23 +747,8 @@ __global__ void __maxnreg__(128)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          const uint32_t acc0 = q > 0 ? 1u : 0u;
-#pragma unroll
-          for (int i = 0; i < KS; ++i) {
-            const int ncol = (S::LV - i) * NC;
-#pragma unroll
-            for (int bb = 0; bb < MB; ++bb) {
-              const int nsp = (ncol + 255) / 256;
-              const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
-#pragma unroll
-              for (int p0 = 0; p0 < ncol;) {
-                const int np = ncol - p0 < part ? ncol - p0 : part;
-                mma_i8(tmem + bb * S::LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + bb) * kCore) >> 4),
-                       dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), i > 0 ? 1u : acc0);
-                p0 += np;
-              }
-            }
-          }
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
           mma_commit(empty + s);
         }
         __syncwarp();
@@ -846,7 +860,7 @@ __global__ void __maxnreg__(128)
     const int qw = warp & 3;
     double fL[S::LV];
 #pragma unroll
-    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -7 * (L + 2));
+    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -kI8Bits * (L + 2));
     for (int it = 0;; ++it) {
       const int b = it & 1;
       mbar_wait_sleep(meta_full + b, (it >> 1) & 1);
@@ -986,8 +1000,8 @@ int m2l_i8_supported(int n, int tile) {
   return (mb == 1 && tile == 32) || ((mb == 2 || mb == 3) && tile == 16) || (mb >= 2 && tile == 32);
 }
 int m2l_i8_fkeys(int nkq) {
-  // |digit| <= 64: one key adds at most KS * KP * 64^2 to a level accumulator
-  const int64_t per_key = (int64_t)kI8Digits * 2 * nkq * 4096;
+  // |digit| <= kI8DigitMax: one key adds at most KS * KP * max^2 to a level accumulator
+  const int64_t per_key = (int64_t)kI8Digits * 2 * nkq * kI8DigitMax * kI8DigitMax;
   const int64_t f = (int64_t)0x7fffffff / per_key;
   return (int)std::min<int64_t>(256, f);
 }
@@ -1010,6 +1024,15 @@ void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_le
   k_mom_max<<<nb, 128, 0, st>>>(mom, slot_level, n, n_pad, lvmax_v, nslots);
   k_mom_quant<kI8Digits><<<nb, 128, 0, st>>>(mom, slot_level, lvmax_v, n, n_pad, nkq, Mq, nslots);
 }
+// pipeline depth: as many K-chunk stages as fit in shared memory beside `reserve`
+// bytes (item tables, barriers, static shared), at most 8
+constexpr int kSmemMax = 232448;
+constexpr int nst_fit(int mb, int tt, int reserve) {
+  const int stage = kI8Digits * mb * kCore + kI8Digits * 2 * tt * kKC;
+  const int n = (kSmemMax - reserve) / stage;
+  return n > 8 ? 8 : (n < 3 ? 3 : n);
+}
+
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
   const int mb = (n + 127) / 128;
@@ -1024,42 +1047,46 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   const bool pipe = pipe_env >= 0 ? pipe_env == 1 : !(mb == 1 && a.pair_out == nullptr);
   // passes over the item list (m2l_i8_passes): one per M-block group; a.counter
   // holds one zeroed claim counter per pass (and per segment)
+  constexpr int kResP = 4096;  // barriers + static shared + alignment (k_m2l_i8p)
   if (pipe) {
     if (mb == 1 && tile == 32) {
-      run_i8p<1, 32, 5, 8>(st, a, 1, 0, 0);
+      run_i8p<1, 32, nst_fit(1, 32, kResP), 8>(st, a, 1, 0, 0);
     } else if (mb == 2 && tile == 16) {
-      run_i8p<2, 16, 3, 8>(st, a, 2, 0, 0);
+      run_i8p<2, 16, nst_fit(2, 16, kResP), 8>(st, a, 2, 0, 0);
     } else if (mb == 3 && tile == 16) {
-      run_i8p<2, 16, 3, 8>(st, a, 3, 0, 0);
-      run_i8p<1, 16, 6, 8>(st, a, 3, 2, 1);
+      run_i8p<2, 16, nst_fit(2, 16, kResP), 8>(st, a, 3, 0, 0);
+      run_i8p<1, 16, nst_fit(1, 16, kResP), 8>(st, a, 3, 2, 1);
     } else if (mb >= 2 && tile == 32) {
-      for (int b = 0; b < mb; ++b) run_i8p<1, 32, 5, 8>(st, a, mb, b, b);
+      for (int b = 0; b < mb; ++b) run_i8p<1, 32, nst_fit(1, 32, kResP), 8>(st, a, mb, b, b);
     } else {
       return 1;
     }
     return 0;
   }
+  // k_m2l_i8 keeps per-item tables of fkeys x (TT + 1) int32 beside the ring
+  constexpr int kFkMax = 256;
+  if (a.fkeys > kFkMax) return 1;
   if (mb == 1 && tile == 32) {
-    run_i8<1, 32, 4, 8, 1>(st, a, 1, 0, 0);
+    constexpr int R = kResP + kFkMax * 33 * 4;
+    if (i8_smem<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8>(a.fkeys) + 2048 <= (size_t)kSmemMax)
+      run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, 1>(st, a, 1, 0, 0);
+    else
+      run_i8<1, 32, nst_fit(1, 32, R), 8, 1>(st, a, 1, 0, 0);
   } else if (mb == 2 && tile == 16) {
-    run_i8<2, 16, 3, 8, 1>(st, a, 2, 0, 0);
+    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 2, 0, 0);
   } else if (mb == 3 && tile == 16) {
-    // 352 rows (m = 6): TMEM holds 7 levels x 32 columns for two M-blocks only, so
+    // 352 rows (m = 6): TMEM holds the levels x 32 columns for two M-blocks only, so
     // the rows run as two M-block groups {0, 1} and {2}, each its own pass over the
     // items with its own ticket chain (same moment gather, disjoint W and rows)
-    run_i8<2, 16, 3, 8, 1>(st, a, 3, 0, 0);
-    run_i8<1, 16, 4, 8, 1>(st, a, 3, 2, 1);
+    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 3, 0, 0);
+    run_i8<1, 16, nst_fit(1, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 3, 2, 1);
   } else if (mb >= 2 && tile == 32) {
-    // 32 target columns (N up to 448 per W digit): one 128-row M-block per pass;
-    // 5 stages fit beside the m = 5, 6 item tables (fkeys <= 128)
-    static const int nst = [] {
-      const char* e = std::getenv("FDH_I8_NST");
-      return e ? std::atoi(e) : 5;
-    }();
-    const bool five = nst == 5 && i8_smem<1, 32, 5, 8>(a.fkeys) + 2048 <= 232448;  // + static shared (aligned)
+    // 32 target columns: one 128-row M-block per pass
     for (int b = 0; b < mb; ++b) {
-      if (five) run_i8<1, 32, 5, 8, 1>(st, a, mb, b, b);
-      else run_i8<1, 32, 4, 8, 1>(st, a, mb, b, b);
+      if (i8_smem<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8>(a.fkeys) + 2048 <= (size_t)kSmemMax)
+        run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, 1>(st, a, mb, b, b);
+      else
+        run_i8<1, 32, nst_fit(1, 32, kResP + kFkMax * 33 * 4), 8, 1>(st, a, mb, b, b);
     }
   } else {
     return 1;

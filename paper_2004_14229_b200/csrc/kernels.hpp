@@ -58,10 +58,34 @@ struct M2LArgs {
 int launch_m2l_gemm(cudaStream_t st, int n_pad, int n_k, int tile, const M2LArgs& a);
 
 // ---- k_m2l_i8.cu: M2L on tcgen05 int8 tensor cores (exact fixed-point digit products)
+// Fixed-point format of the digit products: kI8Digits balanced digits of kI8Bits bits.
+//   6 x 8 (default): base-256 digits in [-128, 127], 48 bits, 21 digit-pair products
+//   7 x 7          : base-128 digits in [-64, 64],   49 bits, 28 products (round 1 / early round 2)
+//   7 x 8          : 56 bits, 28 products (wider margin at the 7 x 7 cost)
 #ifndef FDH_I8_DIGITS
-#define FDH_I8_DIGITS 7
+#define FDH_I8_DIGITS 6
 #endif
-constexpr int kI8Digits = FDH_I8_DIGITS;  // base-128 digits per FP64 value (7 x 7 = 49 bits)
+#ifndef FDH_I8_BITS
+#define FDH_I8_BITS 8
+#endif
+// Digit pairs (i, j) with i + j <= kI8Levels - 1 are kept.  Default for 6 x 8: one level
+// more than digits (26 products: the five level-6 pairs would otherwise dominate the error,
+// ~6x the 48-bit rounding; same operand bytes, one more TMEM level block).
+#ifndef FDH_I8_LEVELS
+#define FDH_I8_LEVELS (FDH_I8_BITS == 8 && FDH_I8_DIGITS == 6 ? 7 : FDH_I8_DIGITS)
+#endif
+constexpr int kI8Digits = FDH_I8_DIGITS;
+constexpr int kI8Bits = FDH_I8_BITS;
+constexpr int kI8Levels = FDH_I8_LEVELS;
+static_assert(kI8Levels >= kI8Digits && kI8Levels <= 2 * kI8Digits - 1, "levels");
+// digit-pair products kept: sum over W digits i of min(KS, LV - i) B digits
+constexpr int i8_products() {
+  int s = 0;
+  for (int i = 0; i < kI8Digits; ++i) s += (kI8Levels - i < kI8Digits ? kI8Levels - i : kI8Digits);
+  return s;
+}
+static_assert(kI8Bits == 7 || kI8Bits == 8, "int8 digits");
+constexpr int kI8DigitMax = 1 << (kI8Bits - 1);  // |digit| <= 64 (7 bits) / 128 (8 bits)
 struct M2LI8Args {
   int n_item = 0, item0 = 0;
   const int32_t *item_tile = nullptr, *item_seq = nullptr;

@@ -10,6 +10,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <atomic>
 #include <memory>
 #include <chrono>
@@ -482,7 +483,7 @@ void build_worklists(Plan& P) {
 // red_ptr / red_idx: per target slot its pair indices (relative to the first
 // pair tile: (tile - pair_tile0) * TT + column), increasing.
 void append_pair_part(Plan& P, std::vector<std::array<int32_t, 3>>& kts, int TT) {
-  std::sort(kts.begin(), kts.end());
+  __gnu_parallel::sort(kts.begin(), kts.end());  // up to 6e8 triples (config 4 hybrid)
   const int64_t np = (int64_t)kts.size();
   const int64_t tile0 = (int64_t)P.tile_level.size(), item0 = (int64_t)P.item_tile.size();
   P.m2l_pair_tile0 = tile0;
@@ -644,34 +645,49 @@ void build_m2l(Plan& P) {
     // 0.45: clustered sources), the M2L runs key-major on (target, source) PAIRS
     // instead (pair mode below): every column carries a key.
     const int64_t w32 = 32 / R, w16 = 16 / R;
-    std::vector<std::pair<int64_t, int64_t>> smp;  // [begin, end) into ts of sampled 32-wide tiles
-    for (size_t i = 0; i < ts.size();) {
-      size_t j = i;
-      const int64_t g = gkey(ts[i]);
-      while (j < ts.size() && gkey(ts[j]) == g) ++j;
-      int64_t q = 0;
-      for (size_t k = i; k < j; k += w32, ++q)
-        if ((q & 7) == 0) smp.push_back({(int64_t)k, (int64_t)std::min(j, k + w32)});
-      i = j;
-    }
-    int64_t k16 = 0, k32 = 0, pairs_s = 0;
-#pragma omp parallel for schedule(dynamic, 16) reduction(+ : k16, k32, pairs_s)
-    for (int64_t si = 0; si < (int64_t)smp.size(); ++si) {
-      const int64_t b = smp[si].first, e = smp[si].second;
-      const int l = T.slot_level[ts[b]];
-      const int32_t kb = key_lo[l], kr = key_hi[l] - kb;
-      thread_local std::vector<uint8_t> mk;
-      mk.assign(kr, 0);
-      for (int64_t i = b; i < e; ++i) {
-        const uint8_t bit = (i - b) < w16 ? 1 : 2;
-        pairs_s += (ptr[ts[i] + 1] - ptr[ts[i]]) * R;
-        for (int64_t q = ptr[ts[i]]; q < ptr[ts[i] + 1]; ++q) mk[sk[q] - kb] |= bit;
+    // sampled cost of an order `ord` of the slots: tile-keys of the 32- and 16-wide
+    // tilings, pairs, and for the 32-wide tiling the full rows / partial pairs of the
+    // hybrid split
+    struct Smp { int64_t k16 = 0, k32 = 0, pairs = 0, full32 = 0, part32 = 0; };
+    auto sample = [&](const std::vector<int32_t>& ord) {
+      std::vector<std::pair<int64_t, int64_t>> smp;  // [begin, end) into ord of sampled 32-wide tiles
+      for (size_t i = 0; i < ord.size();) {
+        size_t j = i;
+        const int64_t g = gkey(ord[i]);
+        while (j < ord.size() && gkey(ord[j]) == g) ++j;
+        int64_t q = 0;
+        for (size_t k = i; k < j; k += w32, ++q)
+          if ((q & 7) == 0) smp.push_back({(int64_t)k, (int64_t)std::min(j, k + w32)});
+        i = j;
       }
-      for (int32_t k = 0; k < kr; ++k) {
-        k32 += mk[k] != 0;
-        k16 += (mk[k] & 1) + (mk[k] >> 1);
+      int64_t k16 = 0, k32 = 0, pairs_s = 0, full32 = 0, part32 = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : k16, k32, pairs_s, full32, part32)
+      for (int64_t si = 0; si < (int64_t)smp.size(); ++si) {
+        const int64_t b = smp[si].first, e = smp[si].second;
+        const int l = T.slot_level[ord[b]];
+        const int32_t kb = key_lo[l], kr = key_hi[l] - kb;
+        thread_local std::vector<uint8_t> mk, ct;
+        mk.assign(kr, 0);
+        ct.assign(kr, 0);
+        for (int64_t i = b; i < e; ++i) {
+          const uint8_t bit = (i - b) < w16 ? 1 : 2;
+          pairs_s += (ptr[ord[i] + 1] - ptr[ord[i]]) * R;
+          for (int64_t q = ptr[ord[i]]; q < ptr[ord[i] + 1]; ++q) {
+            mk[sk[q] - kb] |= bit;
+            ++ct[sk[q] - kb];
+          }
+        }
+        for (int32_t k = 0; k < kr; ++k) {
+          k32 += mk[k] != 0;
+          k16 += (mk[k] & 1) + (mk[k] >> 1);
+          if (ct[k] == e - b) ++full32;
+          else part32 += ct[k] * R;
+        }
       }
-    }
+      return Smp{k16, k32, pairs_s, full32, part32};
+    };
+    const Smp sm = sample(ts);
+    const int64_t k16 = sm.k16, k32 = sm.k32, pairs_s = sm.pairs;
     if (TT < 0) TT = (32.0 * (double)k32 / 1.16 < 16.0 * (double)k16) ? 32 : 16;
     const double useful = (double)pairs_s / std::max(1.0, (double)(TT == 32 ? k32 : k16) * TT);
     const char* pm = std::getenv("FDH_M2L_PAIR");  // 1: force pair mode, 0: never
@@ -897,7 +913,7 @@ void build_m2l(Plan& P) {
   // int8 digits (k_m2l_i8): 7 x ceil(n/128) x 128 x 2 n_kq bytes per key; longer
   // items amortise its per-item TMEM epilogue (config 2: 12 MB 30.2 ms, 24-48 MB 29.1 ms)
   const int nkq = (P.n + 15) / 16 * 16;
-  const int64_t wbytes = P.prm.m2l_impl == 1 ? (int64_t)7 * ((P.n + 127) / 128) * 128 * 2 * nkq
+  const int64_t wbytes = P.prm.m2l_impl == 1 ? (int64_t)P.prm.i8_digits * ((P.n + 127) / 128) * 128 * 2 * nkq
                                               : (int64_t)P.n_pad * m2l_wplanes(P.n_pad) * P.n_k * 8;
   // int8: 48 MB (profiles/r02_m2l_sweep_tt_chunk.jsonl: 2-3 % faster than 24 MB on configs 3, 5
   // and the m = 6 shape); DMMA: optimum 8-12 MB (profiles/r01_m2l_chunk_sweep.txt)

@@ -38,6 +38,7 @@ struct PlanParams {
   int tile = 16;       // M2L target slots per tile
   int m2l_impl = 0;    // 0: FP64 DMMA (k_m2l_gemm), 1: int8 tcgen05 digits (k_m2l_i8)
   int m2l_fkeys = 0;   // > 0: at most this many keys per M2L work item
+  int i8_digits = 7;   // int8 M2L: digits per FP64 value (W bytes per key; set by the C-ABI layer)
   int nrhs = 1;        // right-hand sides per apply: an M2L tile
                        // column is a (target slot, rhs) pair, slot id r * nslots + slot
   int rank = 0, world = 1;

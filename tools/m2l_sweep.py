@@ -63,7 +63,8 @@ def main():
                 for _ in range(a.applies):
                     op.apply(q)
                 st = op.stats()
-                alg = 28.0 * 8.0 * n * n * st["n_c"]
+                ks = int(st["m2l_i8_digits"])
+                alg = st["m2l_i8_products"] * 8.0 * n * n * st["n_c"]
                 ms = st["m2l_gemm_ms"]
                 print(json.dumps({"work": w, "variant": name, "env": envs, "setup_s": round(setup, 2),
                                   "apply_ms": st["apply_ms_sum"] / max(1, st["applies_collected"]), "m2l_ms": ms,
@@ -71,7 +72,7 @@ def main():
                                   "issued_tops": st["m2l_i8_ops"] / ms / 1e9, "useful": alg / st["m2l_i8_ops"],
                                   "tiles": st["m2l_tiles"], "items": st["m2l_items"], "w_resident": st["w_resident"],
                                   "phases": {k: round(v, 3) for k, v in st["phase_ms"].items()},
-                                  "peak_tops": tops}), flush=True)
+                                  "peak_tops": tops, "digits": f"{ks}x{st['m2l_i8_bits']}"}), flush=True)
                 del op
             except Exception as e:
                 print(json.dumps({"work": w, "variant": name, "error": str(e)}), flush=True)
