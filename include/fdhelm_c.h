@@ -216,7 +216,7 @@ double fdh_fp64_peak_tflops(int kind);
 /* Measured dense tensor peak of the current device in TOPS (kind 0: int8
  * tcgen05.mma kind::i8, M=128 N=256 from shared memory), the roofline
  * denominator of the int8 M2L kernel (k_m2l_i8). */
-double fdh_tensor_peak_tops(int kind);
+double fdh_tensor_peak_tops(int kind); /* kind 0: burst (~1 ms), 1: sustained (held ~3 s, power-limited clocks) */
 
 #ifdef __cplusplus
 }

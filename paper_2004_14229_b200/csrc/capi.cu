@@ -449,7 +449,7 @@ void setup_device(fdh_op* o) {
     // apply into a 2-slot ring in segments of key chunks (config 4: 229 GB)
     o->i8 = true;
     o->nkq = (P.n + 15) / 16 * 16;
-    const int64_t wkq = m2l_i8_wbytes_per_key(P.n, o->nkq);
+    const int64_t wkq = m2l_i8_wbytes_per_key(P.n, o->nkq, P.prm.tile);
     const int64_t mq = m2l_i8_mbytes_per_slot(o->nkq) * P.S.nslots * R;
     o->w_resident = !force_otf && (double)(wkq * nkeys + mq) <= 0.7 * (double)fre;
     if (!o->w_resident && (double)mq > 0.3 * (double)fre) throw PlanError{-1, "int8 moment digits do not fit"};
@@ -677,7 +677,7 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
       if (P.m2l_pair)
         CK(cudaMemcpyAsync(o->red_cur, o->red_ptr, sizeof(int64_t) * (size_t)P.T.nslots, cudaMemcpyDeviceToDevice,
                            st));
-      const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq);
+      const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq, P.prm.tile);
       const int64_t ip0 = P.m2l_pair_item0;
       int wslot = -1;
       int64_t wkey0 = -1;  // first key of the digits in the current W slot

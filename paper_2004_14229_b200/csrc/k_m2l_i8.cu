@@ -46,6 +46,9 @@
 #ifndef FDH_I8_BALANCED
 #define FDH_I8_BALANCED 1  // split N > 256 into equal MMAs (0: 256 + rest; tools/gpu_i8_split.sh: ~1 % on config 2)
 #endif
+#ifndef FDH_I8P_G
+#define FDH_I8P_G 1  // k_m2l_i8p: moment-gather stages in flight per warp (beyond the one being issued)
+#endif
 #ifndef FDH_I8_EXP
 #define FDH_I8_EXP 0  // timing experiments: 1 = no B gather, 2 = no W copy, 3 = neither (wrong results)
 #endif
@@ -72,6 +75,13 @@ __host__ __device__ constexpr uint32_t idesc_i8(int n) {
 __host__ __device__ __forceinline__ int core_off(int r, int k) {
   return ((r >> 3) * 2 + (k >> 4)) * 128 + (r & 7) * 16 + (k & 15);
 }
+// rows stored per digit of M-block b / per (key, K chunk) in the trimmed layout
+__host__ __device__ __forceinline__ int i8_rows_of_block(int n, int b) {
+  const int n_pad = (n + 31) / 32 * 32;
+  const int r = n_pad - 128 * b;
+  return r < 128 ? r : 128;
+}
+__host__ __device__ __forceinline__ int i8_rows_total(int n) { return (n + 31) / 32 * 32; }
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -224,13 +234,18 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
     // other, digit-major inside a group -- the M-block passes of launch_m2l_i8
     const int b = j >> 7, rr = j & 127;
     const int g = b / gs, bg = b % gs, mbg = min(gs, mb - gs * g);
+    // gs = 1 (one M-block per pass): the last block stores only its n_pad - 128 (mb - 1)
+    // rows per digit (a prefix of the canonical block: 8-row groups of 256 B)
+    const int rows_tot = gs == 1 ? i8_rows_total(n) : mb * 128;
+    const int dstr = gs == 1 ? i8_rows_of_block(n, b) * kKC : mbg * kCore;  // digit stride
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int kk = h ? nkq + k : k;  // K index: [Re A | Im A]
       const int ch = kk / kKC, kin = kk % kKC;
-      int8_t* base = Wq + (((key - key_base) * nch + ch) * KS * mb + gs * g * KS + bg) * (int64_t)kCore + core_off(rr, kin);
+      int8_t* base = Wq + ((key - key_base) * nch + ch) * (int64_t)(KS * rows_tot * kKC) +
+                     (int64_t)(gs * g * KS + bg) * kCore + core_off(rr, kin);
 #pragma unroll
-      for (int i = 0; i < KS; ++i) base[(int64_t)i * mbg * kCore] = h ? di[i] : dr[i];
+      for (int i = 0; i < KS; ++i) base[(int64_t)i * dstr] = h ? di[i] : dr[i];
     }
   }
   if (!pass) {
@@ -300,38 +315,41 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
 // The MMAs of one pipeline stage (K = 32): W digit i (M-block b) times the stacked
 // B digits j = 0 .. min(KS, LV - i) - 1, into the level blocks i .. (D column =
 // L * NC + target column); N > 256 splits into equal parts (multiples of 32).
+// dstr16: stride between the W digit blocks of a stage in 16-byte units (4096 / 16, or
+// less for a trimmed last M-block: the MMA then reads stale rows >= n_pad, whose output
+// rows are never read).
 // `first`: the item's first stage overwrites -- every level block by the MMA of
 // the first W digit that touches it (level L by i = max(0, L - KS + 1)).
 template <int MB, int KS, int LV, int NC>
 __device__ __forceinline__ void issue_range(uint32_t tmem, uint64_t dA, uint64_t dB, int i, int b, int c0, int c1,
-                                            uint32_t acc) {
+                                            uint32_t acc, uint32_t dstr16) {
   const int ncol = c1 - c0;
   const int nsp = (ncol + 255) / 256;
   const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
 #pragma unroll
   for (int p0 = c0; p0 < c1;) {
     const int np = c1 - p0 < part ? c1 - p0 : part;
-    mma_i8(tmem + b * LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
+    mma_i8(tmem + b * LV * NC + i * NC + p0, dA + (uint64_t)((i * MB + b) * dstr16),
            dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), acc);
     p0 += np;
   }
 }
 template <int MB, int KS, int LV, int NC, bool FIRST>
-__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t dA, uint64_t dB) {
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t dA, uint64_t dB, uint32_t dstr16) {
 #pragma unroll
   for (int i = 0; i < KS; ++i) {
     const int nj = LV - i < KS ? LV - i : KS;  // B digits of W digit i
 #pragma unroll
     for (int b = 0; b < MB; ++b) {
       if (!FIRST) {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u, dstr16);
       } else if (i == 0) {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 0u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 0u, dstr16);
       } else if (i + KS - 1 < LV) {  // this digit is the first to touch level i + KS - 1 (j = KS - 1)
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, (nj - 1) * NC, 1u);
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, (nj - 1) * NC, nj * NC, 0u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, (nj - 1) * NC, 1u, dstr16);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, (nj - 1) * NC, nj * NC, 0u, dstr16);
       } else {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u, dstr16);
       }
     }
   }
@@ -373,7 +391,8 @@ __global__ void __maxnreg__(128)
              const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
              double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
              int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int fkeys, int mb_tot,
-             int blk0, int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out) {
+             int blk0, int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out, int wkc, int wst_bytes,
+             uint32_t dstr16) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int NT = S::THREADS;
@@ -472,10 +491,10 @@ __global__ void __maxnreg__(128)
           if (FDH_I8_EXP & 2) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
           } else {
-            mbar_expect_tx(full + s, S::WST);
+            mbar_expect_tx(full + s, wst_bytes);
             bulk_g2s(wst + s * S::WST,
-                     Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (KS * mb_tot * kCore) + blk0 * (KS * kCore),
-                     S::WST, full + s);
+                     Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore), wst_bytes,
+                     full + s);
           }
         }
         __syncwarp();
@@ -498,8 +517,8 @@ __global__ void __maxnreg__(128)
           // operand offset below is a compile-time constant added to the stage base
           // (keeps the issuing thread at ~3 instructions per MMA)
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
-          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB, dstr16);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB, dstr16);
           mma_commit(empty + s);
         }
         __syncwarp();
@@ -645,7 +664,8 @@ __global__ void __maxnreg__(128)
               const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
               double* __restrict__ tile_acc, int* __restrict__ ticket, double* __restrict__ loc,
               int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int mb_tot, int blk0,
-              int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out) {
+              int tick_off, int64_t key_base, int nrhs, double* __restrict__ pair_out, int wkc, int wst_bytes,
+              uint32_t dstr16) {
   using S = I8Shape<MB, TT, KS, NST, NGW>;
   constexpr int NC = S::NC;
   constexpr int EW0 = 2 + NGW;  // first epilogue warp
@@ -711,10 +731,9 @@ __global__ void __maxnreg__(128)
         const int s = qg % NST;
         if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
         if (lane == 0) {
-          mbar_expect_tx(full + s, S::WST);
-          bulk_g2s(wst + s * S::WST,
-                   Wq + (((int64_t)key - key_base) * nch + ch) * (KS * mb_tot * kCore) + blk0 * (KS * kCore), S::WST,
-                   full + s);
+          mbar_expect_tx(full + s, wst_bytes);
+          bulk_g2s(wst + s * S::WST, Wq + (((int64_t)key - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore),
+                   wst_bytes, full + s);
         }
         __syncwarp();
         if (++ch == nch) {
@@ -747,8 +766,8 @@ __global__ void __maxnreg__(128)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
-          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB, dstr16);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB, dstr16);
           mma_commit(empty + s);
         }
         __syncwarp();
@@ -765,7 +784,9 @@ __global__ void __maxnreg__(128)
     constexpr int RND = (KS * 4 + 7) / 8;
     constexpr int U = (TT / 4) * RND;
     constexpr int UPW = (U + NGW - 1) / NGW;
-    constexpr int G = 1;
+    // cp.async groups (stages) in flight per gather warp beyond the one being issued
+    constexpr int G = FDH_I8P_G < NST - 1 ? FDH_I8P_G : NST - 2;
+    static_assert(G >= 1, "gather depth");
     int dsto[UPW], gofs[UPW], ccol[UPW];
     {
       const int cl = lane >> 3, p8 = lane & 7;
@@ -946,8 +967,19 @@ size_t i8p_smem() {
   return (size_t)NST * S::STAGE + (3 * NST + 6) * 8 + 16;
 }
 
+inline int m2l_i8_wgroup_of(int mb, int tile) { return (tile == 16 && mb >= 2) ? 2 : 1; }
+// W addressing of one pass: bytes per (key, K chunk), bytes per stage, digit stride / 16
+struct WPass { int wkc, wst; uint32_t dstr16; };
+template <int MB>
+WPass wpass(const M2LI8Args& a, int mb_tot, int blk0, bool trimmed) {
+  if (!trimmed) return {kI8Digits * mb_tot * kCore, kI8Digits * MB * kCore, (uint32_t)(kCore >> 4)};
+  const int rows = std::min(128, a.n_pad - 128 * blk0);  // MB == 1
+  return {kI8Digits * a.n_pad * kKC, kI8Digits * rows * kKC, (uint32_t)((rows * kKC) >> 4)};
+}
+
 template <int MB, int TT, int NST, int NGW>
 void run_i8p(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass) {
+  const WPass w = wpass<MB>(a, mb_tot, blk0, m2l_i8_wgroup_of(mb_tot, TT) == 1);
   auto kern = k_m2l_i8p<MB, TT, kI8Digits, NST, NGW>;
   const size_t sm = i8p_smem<MB, TT, NST, NGW>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -962,7 +994,7 @@ void run_i8p(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass
                                             a.tile_tslot, a.tile_level, a.tile_keys, a.tile_src, a.tile_cols,
                                             a.tile_cnt, a.Wq, a.Mq, a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc,
                                             a.counter + pass, a.item0, a.n_item, a.nkq, a.n_pad, mb_tot, blk0,
-                                            pass * a.n_tile, a.key_base, a.nrhs, a.pair_out);
+                                            pass * a.n_tile, a.key_base, a.nrhs, a.pair_out, w.wkc, w.wst, w.dstr16);
 }
 
 template <int MB, int TT, int NST, int NGW>
@@ -973,6 +1005,7 @@ size_t i8_smem(int fkeys) {
 
 template <int MB, int TT, int NST, int NGW, int G>
 void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass) {
+  const WPass w = wpass<MB>(a, mb_tot, blk0, m2l_i8_wgroup_of(mb_tot, TT) == 1);
   using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
   auto kern = k_m2l_i8<MB, TT, kI8Digits, NST, NGW, G>;
   const size_t sm = i8_smem<MB, TT, NST, NGW>(a.fkeys);
@@ -990,7 +1023,7 @@ void run_i8(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass)
                                      a.tile_level, a.tile_keys, a.tile_src, a.tile_cols, a.tile_cnt, a.Wq, a.Mq,
                                      a.lvmax_w, a.lvmax_v, a.tile_acc, a.ticket, a.loc, a.counter + pass, a.item0,
                                      a.n_item, a.nkq, a.n_pad, a.fkeys, mb_tot, blk0, pass * a.n_tile, a.key_base,
-                                     a.nrhs, a.pair_out);
+                                     a.nrhs, a.pair_out, w.wkc, w.wst, w.dstr16);
 }
 
 }  // namespace
@@ -1005,7 +1038,10 @@ int m2l_i8_fkeys(int nkq) {
   const int64_t f = (int64_t)0x7fffffff / per_key;
   return (int)std::min<int64_t>(256, f);
 }
-int64_t m2l_i8_wbytes_per_key(int n, int nkq) { return (int64_t)kI8Digits * ((n + 127) / 128) * kCore * (2 * nkq / kKC); }
+int64_t m2l_i8_wbytes_per_key(int n, int nkq, int tile) {
+  const int rows = m2l_i8_wgroup(n, tile) == 1 ? i8_rows_total(n) : (n + 127) / 128 * 128;  // trimmed last M-block
+  return (int64_t)kI8Digits * rows * kKC * (2 * nkq / kKC);
+}
 int64_t m2l_i8_mbytes_per_slot(int nkq) { return (int64_t)kI8Digits * 2 * 2 * nkq; }
 
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
@@ -1032,6 +1068,8 @@ constexpr int nst_fit(int mb, int tt, int reserve) {
   const int n = (kSmemMax - reserve) / stage;
   return n > 8 ? 8 : (n < 3 ? 3 : n);
 }
+
+constexpr int gdepth(int nst) { return FDH_I8P_G < nst - 1 ? FDH_I8P_G : nst - 2; }
 
 int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (a.n_item <= 0) return 0;
@@ -1069,24 +1107,24 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   if (mb == 1 && tile == 32) {
     constexpr int R = kResP + kFkMax * 33 * 4;
     if (i8_smem<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8>(a.fkeys) + 2048 <= (size_t)kSmemMax)
-      run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, 1>(st, a, 1, 0, 0);
+      run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, gdepth(nst_fit(1, 32, kResP + 128 * 33 * 4))>(st, a, 1, 0, 0);
     else
-      run_i8<1, 32, nst_fit(1, 32, R), 8, 1>(st, a, 1, 0, 0);
+      run_i8<1, 32, nst_fit(1, 32, R), 8, gdepth(nst_fit(1, 32, R))>(st, a, 1, 0, 0);
   } else if (mb == 2 && tile == 16) {
-    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 2, 0, 0);
+    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, gdepth(nst_fit(2, 16, kResP + kFkMax * 17 * 4))>(st, a, 2, 0, 0);
   } else if (mb == 3 && tile == 16) {
     // 352 rows (m = 6): TMEM holds the levels x 32 columns for two M-blocks only, so
     // the rows run as two M-block groups {0, 1} and {2}, each its own pass over the
     // items with its own ticket chain (same moment gather, disjoint W and rows)
-    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 3, 0, 0);
-    run_i8<1, 16, nst_fit(1, 16, kResP + kFkMax * 17 * 4), 8, 1>(st, a, 3, 2, 1);
+    run_i8<2, 16, nst_fit(2, 16, kResP + kFkMax * 17 * 4), 8, gdepth(nst_fit(2, 16, kResP + kFkMax * 17 * 4))>(st, a, 3, 0, 0);
+    run_i8<1, 16, nst_fit(1, 16, kResP + kFkMax * 17 * 4), 8, gdepth(nst_fit(1, 16, kResP + kFkMax * 17 * 4))>(st, a, 3, 2, 1);
   } else if (mb >= 2 && tile == 32) {
     // 32 target columns: one 128-row M-block per pass
     for (int b = 0; b < mb; ++b) {
       if (i8_smem<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8>(a.fkeys) + 2048 <= (size_t)kSmemMax)
-        run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, 1>(st, a, mb, b, b);
+        run_i8<1, 32, nst_fit(1, 32, kResP + 128 * 33 * 4), 8, gdepth(nst_fit(1, 32, kResP + 128 * 33 * 4))>(st, a, mb, b, b);
       else
-        run_i8<1, 32, nst_fit(1, 32, kResP + kFkMax * 33 * 4), 8, 1>(st, a, mb, b, b);
+        run_i8<1, 32, nst_fit(1, 32, kResP + kFkMax * 33 * 4), 8, gdepth(nst_fit(1, 32, kResP + kFkMax * 33 * 4))>(st, a, mb, b, b);
     }
   } else {
     return 1;
@@ -1127,6 +1165,6 @@ int m2l_i8_passes(int n, int tile) {
   if (tile == 32) return mb;
   return mb > 2 ? 2 : 1;
 }
-int m2l_i8_wgroup(int n, int tile) { return (tile == 16 && (n + 127) / 128 >= 2) ? 2 : 1; }
+int m2l_i8_wgroup(int n, int tile) { return m2l_i8_wgroup_of((n + 127) / 128, tile); }
 
 }  // namespace fdhelm

@@ -111,7 +111,7 @@ void launch_m2l_reduce(cudaStream_t st, int64_t nslots, const int64_t* red_ptr, 
                        int64_t* cursor, const double* out, int64_t p0, int64_t p1, double* loc, int n_pad);
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
-int64_t m2l_i8_wbytes_per_key(int n, int nkq);
+int64_t m2l_i8_wbytes_per_key(int n, int nkq, int tile);
 int64_t m2l_i8_mbytes_per_slot(int nkq);
 // gs: M-blocks per W group (m2l_i8_wgroup)
 void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, int64_t key0, int64_t nkeys,
