@@ -854,28 +854,34 @@ void build_m2l(Plan& P) {
     std::vector<int32_t> nvalid(ntile, 0);
     for (int64_t tl = 0; tl < ntile; ++tl)
       for (int c = 0; c < TT; ++c) nvalid[tl] += P.tile_tslot[tl * TT + c] >= 0;
-    int64_t full_tk = 0, part_pairs = 0;
-    for (int64_t tl = 0; tl < ntile; ++tl)
-      for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
-        if (P.tile_cnt[i] == nvalid[tl]) ++full_tk;
-        else part_pairs += P.tile_cnt[i];
-      }
     // pair-part rate relative to the target tiles: the per-item epilogue and
     // pipeline refill cost ~10 stages of K per item of nch stages (measured:
     // m = 4 0.44, m = 5 0.58, m = 6 0.69 -- profiles/r02_m2l_pair_mode.jsonl, _hybrid.jsonl)
     const double nch = 2.0 * ((P.n + 15) / 16 * 16) / 32.0, rate = nch / (nch + 10.0);
+    // a (tile, key) row stays in its target tile when every valid column is present,
+    // or when its pairs would cost more in the pair part (cnt / rate) than the full
+    // row costs in the tile (TT columns, the absent ones zero)
+    auto keep = [&](int64_t i, int64_t tl) {
+      return P.tile_cnt[i] == nvalid[tl] || (double)P.tile_cnt[i] >= rate * (double)TT;
+    };
+    int64_t full_tk = 0, part_pairs = 0;
+    for (int64_t tl = 0; tl < ntile; ++tl)
+      for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
+        if (keep(i, tl)) ++full_tk;
+        else part_pairs += P.tile_cnt[i];
+      }
     const double c_tile = (double)tot * TT, c_hyb = (double)full_tk * TT + (double)part_pairs / rate;
     const char* hm = std::getenv("FDH_M2L_HYBRID");  // 1: force, 0: never
     const bool hybrid = part_pairs > 0 && (hm ? hm[0] == '1' : c_hyb < 0.95 * c_tile);
     if (mdbg)
-      std::fprintf(stderr, "[m2l] hybrid: full tile-keys %lld of %lld, partial pairs %lld, cost %.3g vs %.3g -> %s\n",
+      std::fprintf(stderr, "[m2l] hybrid: kept tile-keys %lld of %lld, pairs moved %lld, cost %.3g vs %.3g -> %s\n",
                    (long long)full_tk, (long long)tot, (long long)part_pairs, c_hyb, c_tile, hybrid ? "yes" : "no");
     if (hybrid) {
       hyb.reserve(part_pairs);
       std::vector<int64_t> nk(ntile + 1, 0);
       for (int64_t tl = 0; tl < ntile; ++tl) {
         for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
-          if (P.tile_cnt[i] == nvalid[tl]) {
+          if (keep(i, tl)) {
             ++nk[tl + 1];
             continue;
           }
@@ -887,7 +893,7 @@ void build_m2l(Plan& P) {
       int64_t w = 0;  // compact the kept (tile, key) rows in place (order preserved)
       for (int64_t tl = 0; tl < ntile; ++tl)
         for (int64_t i = P.tile_kptr[tl]; i < P.tile_kptr[tl + 1]; ++i) {
-          if (P.tile_cnt[i] != nvalid[tl]) continue;
+          if (!keep(i, tl)) continue;
           if (w != i) {
             P.tile_keys[w] = P.tile_keys[i];
             P.tile_cnt[w] = P.tile_cnt[i];
