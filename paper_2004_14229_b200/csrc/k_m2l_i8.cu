@@ -9,24 +9,26 @@
 // in complex128.  tcgen05 has no f64 kind, so the FP64 product is computed
 // EXACTLY in integers (Ozaki-style fixed-point slicing):
 //   * W (per tree level, one power-of-two scale S_W = 2^(eW+1) > 2 max|W|) and the
-//     moments v (per level, S_V) are rounded to 7*KS-bit fixed point and split
-//     into KS balanced base-128 digits d_i in [-64, 64] (int8), most significant
-//     first: x = S * sum_i d_i 2^(-7(i+1)) (+ rounding error <= S 2^(-7 KS - 1));
-//   * the product needs only the digit pairs i + j <= LMAX = KS - 1 (the dropped
-//     pairs weigh <= 2^(-7(KS+1)) relative); pairs of one level L = i + j share
-//     the weight 2^(-7(L+2)) and are summed EXACTLY in one int32 TMEM accumulator
-//     column block: one MMA per W digit i multiplies W_i by the B digits
-//     [B_0 | B_1 | ... | B_{LMAX-i}] stacked along N and lands in the level
-//     blocks i .. LMAX (D column = L * 2TT + target column);
+//     moments v (per (rhs, level), S_V) are rounded to B*KS-bit fixed point and split
+//     into KS balanced base-2^B digits (int8), most significant first:
+//     x = S * sum_i d_i 2^(-B(i+1)) (+ rounding error <= S 2^(-B KS - 1)).
+//     Default KS x B = 6 x 8 (d_i in [-128, 127], 48 bits); 7 x 7 and 7 x 8 compile
+//     (kernels.hpp);
+//   * the product keeps the digit pairs i + j <= LV - 1 (default LV = 7: 26 of 36
+//     pairs; the dropped ones weigh <= 2^(-B(LV+2)) 2^14 relative); pairs of one
+//     level L = i + j share the weight 2^(-B(L+2)) and are summed EXACTLY in one
+//     int32 TMEM accumulator column block: one MMA per W digit i multiplies W_i by
+//     the B digits [B_0 | B_1 | ... | B_min(KS, LV - i) - 1] stacked along N and lands
+//     in the level blocks i .. (D column = L * 2TT + target column);
 //   * every key of a (tile, key-chunk) item accumulates into the same TMEM
 //     columns (the scales are per level, hence per tile), so the int32 sums are
 //     exact as long as an item has <= F keys (F from the digit bound, planner);
-//   * the epilogue reads TMEM once per item and forms sum_L acc_L 2^(-7(L+2))
+//   * the epilogue reads TMEM once per item and forms sum_L acc_L 2^(-B(L+2))
 //     S_W S_V in FP64 (fixed order); items of a tile are chained in key-chunk
 //     order as in k_m2l_gemm (deterministic, no FP atomics).
-// Relative error per block ~1e-14 at KS = 7 (vs 1e-12 allowed, north_star):
-// the product is exact, only the 7*KS-bit rounding of W and v and the dropped
-// digit pairs remain.
+// Relative l2 error of y ~3e-14 .. 9e-14 on the BASELINE configs (vs 1e-12 allowed,
+// north_star): the product is exact, only the 48-bit rounding of W and v and the
+// dropped digit pairs remain.
 //
 // Data movement: the digits of W live in HBM pre-arranged in the UMMA canonical
 // K-major layout (core matrices of 8 rows x 16 B, SWIZZLE_NONE), one contiguous
@@ -140,6 +142,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
+}
+// int32 -> double without the conversion unit (I2F.F64 issues at a quarter of the FP64
+// rate and bounded the epilogue): the double with high word 0x43300000 and low word
+// x ^ 2^31 is 2^52 + 2^31 + x exactly; one subtraction leaves x
+__device__ __forceinline__ double i32_to_f64(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)(x ^ 0x80000000u)) - 4503601774854144.0;
 }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -596,7 +604,7 @@ __global__ void __maxnreg__(128)
         for (int e = 0; e < 8; ++e) {
           double a = 0.0;
 #pragma unroll
-          for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
+          for (int L = S::LV - 1; L >= 0; --L) a += i32_to_f64(r[L][e]) * fL[L];
           v[e] = a * csc[(8 * g + e) >> 1];  // exact: a power of two
         }
         double* pa = A + (int64_t)row * NC + 8 * g;
@@ -917,7 +925,7 @@ __global__ void __maxnreg__(128)
           for (int e = 0; e < 8; ++e) {
             double a = 0.0;
 #pragma unroll
-            for (int L = S::LV - 1; L >= 0; --L) a += (double)(int32_t)r[L][e] * fL[L];
+            for (int L = S::LV - 1; L >= 0; --L) a += i32_to_f64(r[L][e]) * fL[L];
             v[e] = a * csc[(8 * g + e) >> 1];
           }
           if (pair_out) {
