@@ -115,6 +115,7 @@ struct fdh_op {
   int32_t *key_level = nullptr, *key_dir = nullptr;
   int64_t* key_d = nullptr;
   double *W = nullptr, *mom = nullptr, *loc = nullptr;
+  double* loc2 = nullptr;  // hybrid int8 M2L: the pair part's sums (added to loc after the M2L)
   // int8 tensor-core M2L (k_m2l_i8.cu): digits of W (setup) and of the moments (per apply)
   bool i8 = false;
   int nkq = 0;
@@ -485,21 +486,41 @@ void setup_device(fdh_op* o) {
       if (const char* pb = std::getenv("FDH_PAIR_OUT_MB")) cap_bytes = std::max(1.0, std::atof(pb)) * 1048576.0;
       const int64_t TT = P.prm.tile;
       const int64_t cap_items = std::max<int64_t>(1, (int64_t)(cap_bytes / (16.0 * P.n_pad * TT)));
-      const int ip0 = (int)P.m2l_pair_item0;
-      std::vector<fdh_op::Seg> base = o->segs;
-      if (base.empty()) base.push_back({0, (int)P.item_tile.size(), 0, nkeys, true, false});
+      const int ip0 = (int)P.m2l_pair_item0, ni = (int)P.item_tile.size();
       o->segs.clear();
-      for (const fdh_op::Seg& b : base) {
-        bool first = true;
-        if (b.item0 < ip0) {  // target-tile items of this W segment
-          o->segs.push_back({b.item0, std::min(b.item1, ip0), b.key0, b.key1, first, false});
-          first = false;
+      auto push_pairs = [&](int i0, int i1, int64_t k0, int64_t k1, bool gen) {
+        for (int i = i0; i < i1; i += (int)cap_items) {
+          o->segs.push_back({i, (int)std::min<int64_t>(i1, i + cap_items), k0, k1, gen, true});
+          gen = false;
         }
-        for (int i = std::max(b.item0, ip0); i < b.item1; i += (int)cap_items) {
-          o->segs.push_back({i, (int)std::min<int64_t>(b.item1, i + cap_items), b.key0, b.key1, first, true});
-          first = false;
+      };
+      if (o->w_resident) {
+        if (ip0 > 0) o->segs.push_back({0, ip0, 0, nkeys, false, false});
+        push_pairs(ip0, ni, 0, nkeys, false);
+      } else {
+        // per W slot (key range): its target-tile items, then its pair items, so the
+        // slot's digits are generated once for both parts (both are key-ordered)
+        const int64_t sk = o->w_slot_keys;
+        auto slot_of = [&](int i) { return (int64_t)P.tile_keys[P.item_k0[i]] / sk; };
+        int it = 0, ip = ip0;
+        while (it < ip0 || ip < ni) {
+          const int64_t sl = std::min(it < ip0 ? slot_of(it) : INT64_MAX, ip < ni ? slot_of(ip) : INT64_MAX);
+          const int64_t k0 = sl * sk, k1 = std::min(nkeys, (sl + 1) * sk);
+          bool gen = true;
+          int j = it;
+          while (j < ip0 && slot_of(j) == sl) ++j;
+          if (j > it) {
+            o->segs.push_back({it, j, k0, k1, true, false});
+            gen = false;
+          }
+          it = j;
+          j = ip;
+          while (j < ni && slot_of(j) == sl) ++j;
+          if (j > ip) push_pairs(ip, j, k0, k1, gen);
+          ip = j;
         }
       }
+      if (ip0 > 0) o->loc2 = o->alloc<double>((size_t)(P.T.nslots * 2 * P.n_pad));  // hybrid (one rhs)
       o->pair_out = o->alloc<double>((size_t)(cap_items * TT * 2 * P.n_pad));
       o->red_ptr = o->up(P.red_ptr);
       o->red_idx = o->up(P.red_idx);
@@ -677,6 +698,11 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
       if (P.m2l_pair)
         CK(cudaMemcpyAsync(o->red_cur, o->red_ptr, sizeof(int64_t) * (size_t)P.T.nslots, cudaMemcpyDeviceToDevice,
                            st));
+      // hybrid: the pair part sums into its own buffer (running sum in pair order from 0)
+      // and is added to the tiles' locals once at the end -- the same bits whatever the
+      // order of tile and pair segments (the tiles' last items ASSIGN the locals)
+      double* pair_sum = o->loc2 ? o->loc2 : o->loc;
+      if (o->loc2) CK(cudaMemsetAsync(o->loc2, 0, sizeof(double) * (size_t)lstr, st));
       const int64_t wkq = m2l_i8_wbytes_per_key(n, o->nkq, P.prm.tile);
       const int64_t ip0 = P.m2l_pair_item0;
       int wslot = -1;
@@ -705,9 +731,13 @@ void apply_device(fdh_op* o, const double2* x, double2* y, cudaStream_t st, bool
         L += ng;
         if (S.pair) {
           launch_m2l_reduce(st, P.T.nslots, o->red_ptr, o->red_idx, o->red_cur, o->pair_out,
-                            (S.item0 - ip0) * (int64_t)P.prm.tile, (S.item1 - ip0) * (int64_t)P.prm.tile, o->loc, np);
+                            (S.item0 - ip0) * (int64_t)P.prm.tile, (S.item1 - ip0) * (int64_t)P.prm.tile, pair_sum, np);
           L += 1;
         }
+      }
+      if (o->loc2) {
+        launch_m2l_add(st, o->loc, o->loc2, lstr);
+        L += 2;
       }
       L += 3;
     }

@@ -217,6 +217,11 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
   __syncthreads();
   const int ex = pass ? level_exp(lvmax, l) : 0;
   const int nch = 2 * nkq / kKC;
+  extern __shared__ __align__(16) int8_t sbuf[];  // pass 1: [digit][K chunk][256 B]
+  if (pass) {
+    for (int v = threadIdx.x; v < KS * nch * 16; v += blockDim.x) reinterpret_cast<int4*>(sbuf)[v] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+  }
   double mx = 0.0;
   for (int idx = threadIdx.x; idx < kCplRows * n; idx += blockDim.x) {
     const int j = r0 + idx / n, k = idx % n;
@@ -237,23 +242,35 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
     int8_t dr[KS], di[KS];
     to_digits<KS>(re, ex, dr);
     to_digits<KS>(im, ex, di);
-    // M-block b belongs to group g = b / gs (gs = 2: blocks {0, 1}, {2}; gs = 1: one
-    // block per group); per (key, K chunk) the groups are stored one after the
-    // other, digit-major inside a group -- the M-block passes of launch_m2l_i8
-    const int b = j >> 7, rr = j & 127;
-    const int g = b / gs, bg = b % gs, mbg = min(gs, mb - gs * g);
-    // gs = 1 (one M-block per pass): the last block stores only its n_pad - 128 (mb - 1)
-    // rows per digit (a prefix of the canonical block: 8-row groups of 256 B)
-    const int rows_tot = gs == 1 ? i8_rows_total(n) : mb * 128;
-    const int dstr = gs == 1 ? i8_rows_of_block(n, b) * kKC : mbg * kCore;  // digit stride
+    // staged in shared memory: per (digit, K chunk) the 256 bytes of this CTA's
+    // 8-row group in the canonical layout (2 K halves x 8 rows x 16 B)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int kk = h ? nkq + k : k;  // K index: [Re A | Im A]
       const int ch = kk / kKC, kin = kk % kKC;
-      int8_t* base = Wq + ((key - key_base) * nch + ch) * (int64_t)(KS * rows_tot * kKC) +
-                     (int64_t)(gs * g * KS + bg) * kCore + core_off(rr, kin);
+      int8_t* sb = sbuf + ch * 256 + (kin >> 4) * 128 + (j - r0) * 16 + (kin & 15);
 #pragma unroll
-      for (int i = 0; i < KS; ++i) base[(int64_t)i * dstr] = h ? di[i] : dr[i];
+      for (int i = 0; i < KS; ++i) sb[i * nch * 256] = h ? di[i] : dr[i];
+    }
+  }
+  if (pass) {
+    // M-block b belongs to group g = b / gs (gs = 2: blocks {0, 1}, {2}; gs = 1: one
+    // block per group); per (key, K chunk) the groups are stored one after the
+    // other, digit-major inside a group -- the M-block passes of launch_m2l_i8.
+    // gs = 1 (one M-block per pass): the last block stores only its n_pad - 128 (mb - 1)
+    // rows per digit (a prefix of the canonical block: 8-row groups of 256 B)
+    __syncthreads();
+    const int b = r0 >> 7, rr = r0 & 127;
+    const int g = b / gs, bg = b % gs, mbg = min(gs, mb - gs * g);
+    const int rows_tot = gs == 1 ? i8_rows_total(n) : mb * 128;
+    const int dstr = gs == 1 ? i8_rows_of_block(n, b) * kKC : mbg * kCore;  // digit stride
+    int8_t* base = Wq + (key - key_base) * nch * (int64_t)(KS * rows_tot * kKC) + (int64_t)(gs * g * KS + bg) * kCore +
+                   (rr >> 3) * 256;
+    // coalesced: 16 lanes x 16 B per (digit, chunk) group, padding rows / K as zeros
+    for (int v = threadIdx.x; v < KS * nch * 16; v += blockDim.x) {
+      const int q = v & 15, ic = v >> 4, i = ic / nch, ch = ic - i * nch;
+      *reinterpret_cast<int4*>(base + (int64_t)ch * (KS * rows_tot * kKC) + (int64_t)i * dstr + q * 16) =
+          *reinterpret_cast<const int4*>(sbuf + ic * 256 + q * 16);
     }
   }
   if (!pass) {
@@ -1057,8 +1074,14 @@ void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, 
                         unsigned long long* lvmax, int8_t* Wq, int n, int nkq, int gs, int64_t key_base) {
   if (nkeys <= 0) return;
   dim3 grid((unsigned)nkeys, (unsigned)((n + kCplRows - 1) / kCplRows));
-  k_coupling_i8<kI8Digits><<<grid, 256, 0, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
-                                                 (n + 127) / 128, gs, key_base);
+  const size_t sm = pass ? (size_t)kI8Digits * (2 * nkq / kKC) * 256 : 0;
+  static size_t sm_set = 0;
+  if (sm > 40 * 1024 && sm > sm_set) {  // static shared (node tables) counts towards the 48 KB default
+    cudaFuncSetAttribute(k_coupling_i8<kI8Digits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    sm_set = sm;
+  }
+  k_coupling_i8<kI8Digits><<<grid, 256, sm, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
+                                                  (n + 127) / 128, gs, key_base);
 }
 void launch_mom_quant(cudaStream_t st, const double* mom, const int32_t* slot_level, int64_t nslots, int n, int n_pad,
                       int nkq, unsigned long long* lvmax_v, int8_t* Mq, int nrhs) {
@@ -1166,6 +1189,19 @@ void launch_m2l_reduce(cudaStream_t st, int64_t nslots, const int64_t* red_ptr, 
                        int64_t* cursor, const double* out, int64_t p0, int64_t p1, double* loc, int n_pad) {
   if (nslots <= 0) return;
   k_m2l_reduce<<<(unsigned)nslots, 256, 0, st>>>(red_ptr, red_idx, cursor, out, p0, p1, loc, n_pad);
+}
+
+namespace {
+__global__ void __launch_bounds__(256) k_m2l_add(double* __restrict__ loc, const double* __restrict__ add, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    loc[i] += add[i];
+}
+}  // namespace
+// hybrid mode: locals = target-tile part (assigned by the tiles' last items) + pair part
+// (its own running sum): one fixed addition per entry, whatever the segment order
+void launch_m2l_add(cudaStream_t st, double* loc, const double* add, int64_t n) {
+  if (n <= 0) return;
+  k_m2l_add<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(loc, add, n);
 }
 
 int m2l_i8_passes(int n, int tile) {

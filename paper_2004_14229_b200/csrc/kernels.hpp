@@ -109,6 +109,7 @@ struct M2LI8Args {
 };
 void launch_m2l_reduce(cudaStream_t st, int64_t nslots, const int64_t* red_ptr, const int64_t* red_idx,
                        int64_t* cursor, const double* out, int64_t p0, int64_t p1, double* loc, int n_pad);
+void launch_m2l_add(cudaStream_t st, double* loc, const double* add, int64_t n);
 int m2l_i8_supported(int n, int tile);
 int m2l_i8_fkeys(int nkq);                    // max keys per item (int32 accumulators exact)
 int64_t m2l_i8_wbytes_per_key(int n, int nkq, int tile);
