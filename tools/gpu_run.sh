@@ -7,7 +7,8 @@
 #   tests [pytest -k expr]    pytest -m gpu (optionally filtered)
 #   bench [bench.py args]     one bench line  -> gpurun_out/bench_<tag>.jsonl (tag = $TAG or "run")
 #   ref [bench.py args]       the reference arm (bench.py --impl reference)
-#   launches [bench.py args]  ncu launch list (gpu__time_duration.sum, cold) of a short bench run
+#   launches [bench.py args]  ncu launch list (gpu__time_duration.sum, cold) of a short bench run;
+#                             NCU_EXTRA_METRICS=dram__bytes_read.sum,dram__bytes_write.sum adds DRAM bytes per kernel
 #   ncu <kernel-regex> <count> [bench.py args]   ncu --set full of one kernel from a short bench run
 #   py <script> [args]        any python tool (tools/*.py)
 set -u
@@ -25,7 +26,7 @@ case "$task" in
     echo "bench rc=$?"; tail -c 3000 gpurun_out/bench_$tag.jsonl; tail -5 gpurun_out/bench_$tag.err ;;
   ref) timeout ${BENCH_TIMEOUT:-2400} python bench.py --impl reference "$@" > gpurun_out/ref_$tag.jsonl 2> gpurun_out/ref_$tag.err
     echo "ref rc=$?"; tail -c 2000 gpurun_out/ref_$tag.jsonl; tail -5 gpurun_out/ref_$tag.err ;;
-  launches) timeout ${BENCH_TIMEOUT:-2400} ncu --metrics gpu__time_duration.sum --clock-control none -c ${NCU_COUNT:-2000} --csv \
+  launches) timeout ${BENCH_TIMEOUT:-2400} ncu --metrics gpu__time_duration.sum${NCU_EXTRA_METRICS:+,$NCU_EXTRA_METRICS} --clock-control none -c ${NCU_COUNT:-2000} --csv \
       --log-file gpurun_out/launches_$tag.csv python bench.py --no-cpu-baseline "$@" > gpurun_out/launches_$tag.log 2>&1
     echo "launches rc=$?"; python tools/ncu_summary.py launches gpurun_out/launches_$tag.csv gpurun_out/launches_$tag.json | tail -20 ;;
   ncu) k=$1; c=$2; shift 2

@@ -56,7 +56,7 @@ def report(path):
 def launches(path):
     rows = list(csv.reader(open(path)))
     hdr = None
-    agg = {}
+    agg, dram = {}, {}
     for r in rows:
         if "Kernel Name" in r:
             hdr = r
@@ -64,15 +64,28 @@ def launches(path):
         if hdr is None or len(r) != len(hdr):
             continue
         d = dict(zip(hdr, r))
+        k = d["Kernel Name"].split("(")[0]
+        val = float(d["Metric Value"].replace(",", ""))
+        if d.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            unit = d.get("Metric Unit", "byte")
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
+            dram.setdefault(k, [0.0, 0.0])[0 if "read" in d["Metric Name"] else 1] += val * scale
+            continue
         if d.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        k = d["Kernel Name"].split("(")[0]
-        agg.setdefault(k, []).append(float(d["Metric Value"].replace(",", "")))
+        unit = d.get("Metric Unit", "ns")
+        agg.setdefault(k, []).append(val * {"ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9}.get(unit, 1.0))
     tot = sum(sum(v) for v in agg.values())
     ks = sorted(agg.items(), key=lambda x: -sum(x[1]))
-    return {"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none: cold-cache, serialised",
-            "kernels": [{"kernel": k, "launches": len(v), "total_ms": sum(v) / 1e6, "avg_ms": sum(v) / len(v) / 1e6,
-                         "share": sum(v) / tot} for k, v in ks]}
+    out = []
+    for k, v in ks:
+        e = {"kernel": k, "launches": len(v), "total_ms": sum(v) / 1e6, "avg_ms": sum(v) / len(v) / 1e6,
+             "share": sum(v) / tot}
+        if k in dram:
+            e["dram_read_gb"], e["dram_write_gb"] = dram[k][0] / 1e9, dram[k][1] / 1e9
+        out.append(e)
+    return {"source": path, "note": "ncu --metrics gpu__time_duration.sum[,dram__bytes_*] --clock-control none: "
+                                    "cold-cache, serialised; totals over all launches of the run", "kernels": out}
 
 
 if __name__ == "__main__":
