@@ -6,7 +6,7 @@ A step = one apply y = A x of the configured workload.  Default: BASELINE
 config 4 (N_T = N_S = 4,000,000, kappa = 64, m = 6) -- the scaling config the
 metric is quoted on ("at 1/2/4/8 B200"), the largest that runs on one GPU.
 Setup (trees, partition, coupling scales) is outside the timed region, as t_s in
-PAPER.md Table 1, and reported as config.setup_s.
+PAPER.md Table 1, and reported as run.setup_s.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
@@ -49,6 +49,16 @@ def workload_desc(c):
     return (f"BASELINE config {c.cfg}: N_T={c.nt}, N_S={c.ns}, kappa={c.kappa:g}, degree m={c.m} "
             f"({(c.m + 1) ** 3} nodes/box), n_max={c.n_max}, eta2={c.eta2:g}, default directions, "
             f"root {c.root_lo}-{c.root_hi}{', Gaussian-mixture sources' if c.mixture_sources else ''}")
+
+
+def config_block(c):
+    """`config` of the JSON line: the workload and the L2 statement -- the same dict in both
+    arms (the driver compares them); run-specific facts (parallelism, launch mode, setup
+    seconds) are in `run`."""
+    return {"workload": workload_desc(c), "cfg": c.cfg,
+            "l2": "the apply's working set (coupling matrices / digits, moments: GBs) is far larger than the 126 MB "
+                  "L2 and any CPU cache; the GPU arm also flushes L2 (256 MB write) between timed steps, outside "
+                  "the step events"}
 
 
 class ClockSampler:
@@ -200,7 +210,7 @@ def run_reference(args, c, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "complex128 (f64)", "data": "synthetic (seeded, SURVEY.md 8(d))",
-        "config": {"workload": workload_desc(c), "cfg": c.cfg},
+        "config": config_block(c),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
                          "sample": ref.describe(r, args.steps) + f"; mean over {args.steps} samples (extrapolated)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -397,12 +407,11 @@ def run_ours(args, c, rank, world, local_rank):
         "dtype": (f"complex128 (f64; M2L as exact int8 x int8 -> int32 digit products of "
                   f"{st['m2l_i8_digits'] * st['m2l_i8_bits']}-bit fixed-point operands on tcgen05)" if st["m2l_impl"] == 1 else "complex128 (f64)"),
         "data": "synthetic (seeded uniform / Gaussian-mixture points, U(-1,1) complex charges; SURVEY.md 8(d))",
-        "config": {"workload": workload_desc(c), "cfg": c.cfg, "parallelism": f"target-leaf shards x{world}",
-                   "l2": "flushed between timed steps (256 MB write, outside the step events); the apply's working "
-                         "set (coupling digits, moments) is far larger than L2",
-                   "launch_mode": f"CUDA graph replays ({st['graph_replays']} in total incl. warm-up), phase timing "
-                                  f"by event-record nodes inside the graph",
-                   "setup_s": setup_s},
+        "config": config_block(c),
+        "run": {"parallelism": f"target-leaf shards x{world}",
+                "launch_mode": f"CUDA graph replays ({st['graph_replays']} in total incl. warm-up), phase timing "
+                               f"by event-record nodes inside the graph",
+                "setup_s": setup_s},
         "roofline": roofline_block(st, c, m2l_flops, peak, gemm_ms, ms_per_step, traffic),
         "phases_ms": ph,
         "p2p": {"pairs": st["m_d"], "ms": p2p_ms,

@@ -43,7 +43,7 @@
 #include <cstdlib>
 
 #ifndef FDH_I8_SLEEP_NS
-#define FDH_I8_SLEEP_NS 128  // producer back-off between empty-barrier polls
+#define FDH_I8_SLEEP_NS 0  // > 0: nanosleep polling in the long mbarrier waits (0: try_wait suspend hint)
 #endif
 #ifndef FDH_I8_BALANCED
 #define FDH_I8_BALANCED 1  // split N > 256 into equal MMAs (0: 256 + rest; tools/gpu_i8_split.sh: ~1 % on config 2)
@@ -108,9 +108,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// producer-side wait (the ring is usually ahead): back off between polls so the
-// spinning warps do not steal shared-memory wavefronts from the tensor core
+// long waits (producers ahead of the ring, epilogue warps waiting for an item's MMAs):
+// try_wait with a suspend-time hint -- the warp is parked by the hardware until the
+// phase completes (no wake-up latency) instead of polling every ~30 ns (NANOSLEEP 128
+// returned early: ncu counted 1.6e10 polls per pass, 25 % of all issued instructions,
+// each a shared-memory wavefront beside the tensor core's operand reads).
+// FDH_I8_SLEEP_NS > 0 restores the nanosleep polling loop.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+#if FDH_I8_SLEEP_NS > 0
   uint32_t ok = 0;
   while (true) {
     asm volatile(
@@ -123,12 +128,33 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
     if (ok) return;
     __nanosleep(FDH_I8_SLEEP_NS);
   }
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAITS_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(1000000u)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// one stage of W digits: one bulk copy when the digit blocks are full (src stride =
+// 4096), else KS copies of wdig bytes to the 4096-byte digit slots
+template <int KS>
+__device__ __forceinline__ void w_stage_g2s(uint8_t* dst, const int8_t* src, int wst_bytes, uint32_t wdig,
+                                            uint64_t* bar) {
+  mbar_expect_tx(bar, wst_bytes);
+  if (wdig == (uint32_t)kCore || wdig * KS != (uint32_t)wst_bytes) {
+    bulk_g2s(dst, src, wst_bytes, bar);
+  } else {
+#pragma unroll
+    for (int i = 0; i < KS; ++i) bulk_g2s(dst + i * kCore, src + i * wdig, wdig, bar);
+  }
 }
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -340,41 +366,42 @@ __global__ void __launch_bounds__(128) k_mom_quant(const double* __restrict__ mo
 // The MMAs of one pipeline stage (K = 32): W digit i (M-block b) times the stacked
 // B digits j = 0 .. min(KS, LV - i) - 1, into the level blocks i .. (D column =
 // L * NC + target column); N > 256 splits into equal parts (multiples of 32).
-// dstr16: stride between the W digit blocks of a stage in 16-byte units (4096 / 16, or
-// less for a trimmed last M-block: the MMA then reads stale rows >= n_pad, whose output
-// rows are never read).
+// In shared memory every W digit block is 4096 bytes apart; a trimmed last M-block
+// (fewer than 128 rows stored per digit) is copied digit by digit and its missing rows
+// stay zero in shared memory (zeroed once per CTA: zero operands keep the MMA's power
+// down; their output rows are never read).
 // `first`: the item's first stage overwrites -- every level block by the MMA of
 // the first W digit that touches it (level L by i = max(0, L - KS + 1)).
 template <int MB, int KS, int LV, int NC>
 __device__ __forceinline__ void issue_range(uint32_t tmem, uint64_t dA, uint64_t dB, int i, int b, int c0, int c1,
-                                            uint32_t acc, uint32_t dstr16) {
+                                            uint32_t acc) {
   const int ncol = c1 - c0;
   const int nsp = (ncol + 255) / 256;
   const int part = FDH_I8_BALANCED ? ((ncol / nsp + 31) / 32) * 32 : 256;
 #pragma unroll
   for (int p0 = c0; p0 < c1;) {
     const int np = c1 - p0 < part ? c1 - p0 : part;
-    mma_i8(tmem + b * LV * NC + i * NC + p0, dA + (uint64_t)((i * MB + b) * dstr16),
+    mma_i8(tmem + b * LV * NC + i * NC + p0, dA + (uint64_t)(((i * MB + b) * kCore) >> 4),
            dB + (uint64_t)((p0 * kKC) >> 4), idesc_i8(np), acc);
     p0 += np;
   }
 }
 template <int MB, int KS, int LV, int NC, bool FIRST>
-__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t dA, uint64_t dB, uint32_t dstr16) {
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint64_t dA, uint64_t dB) {
 #pragma unroll
   for (int i = 0; i < KS; ++i) {
     const int nj = LV - i < KS ? LV - i : KS;  // B digits of W digit i
 #pragma unroll
     for (int b = 0; b < MB; ++b) {
       if (!FIRST) {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u, dstr16);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
       } else if (i == 0) {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 0u, dstr16);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 0u);
       } else if (i + KS - 1 < LV) {  // this digit is the first to touch level i + KS - 1 (j = KS - 1)
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, (nj - 1) * NC, 1u, dstr16);
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, (nj - 1) * NC, nj * NC, 0u, dstr16);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, (nj - 1) * NC, 1u);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, (nj - 1) * NC, nj * NC, 0u);
       } else {
-        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u, dstr16);
+        issue_range<MB, KS, LV, NC>(tmem, dA, dB, i, b, 0, nj * NC, 1u);
       }
     }
   }
@@ -435,6 +462,9 @@ __global__ void __maxnreg__(128)
   __shared__ double csc[TT];  // S_W S_V of each tile column (its rhs' moment scale)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kp = 2 * nkq, nch = kp / kKC;
+  // W ring zeroed once: rows a trimmed M-block does not store stay zero operands
+  for (int i = tid * 16; i < NST * S::WST; i += (int)blockDim.x * 16) *reinterpret_cast<int4*>(wst + i) = make_int4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + s, 1);
@@ -516,10 +546,9 @@ __global__ void __maxnreg__(128)
           if (FDH_I8_EXP & 2) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full + s)) : "memory");
           } else {
-            mbar_expect_tx(full + s, wst_bytes);
-            bulk_g2s(wst + s * S::WST,
-                     Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore), wst_bytes,
-                     full + s);
+            w_stage_g2s<KS>(wst + s * S::WST,
+                            Wq + (((int64_t)keys[kq] - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore),
+                            wst_bytes, dstr16 * 16u, full + s);
           }
         }
         __syncwarp();
@@ -542,8 +571,8 @@ __global__ void __maxnreg__(128)
           // operand offset below is a compile-time constant added to the stage base
           // (keeps the issuing thread at ~3 instructions per MMA)
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB, dstr16);
-          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB, dstr16);
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
           mma_commit(empty + s);
         }
         __syncwarp();
@@ -709,6 +738,9 @@ __global__ void __maxnreg__(128)
   __shared__ double csc[TT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kp = 2 * nkq, nch = kp / kKC;
+  // W ring zeroed once: rows a trimmed M-block does not store stay zero operands
+  for (int i = tid * 16; i < NST * S::WST; i += (int)blockDim.x * 16) *reinterpret_cast<int4*>(wst + i) = make_int4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full + s, 1);
@@ -756,9 +788,9 @@ __global__ void __maxnreg__(128)
         const int s = qg % NST;
         if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
         if (lane == 0) {
-          mbar_expect_tx(full + s, wst_bytes);
-          bulk_g2s(wst + s * S::WST, Wq + (((int64_t)key - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore),
-                   wst_bytes, full + s);
+          w_stage_g2s<KS>(wst + s * S::WST,
+                          Wq + (((int64_t)key - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore), wst_bytes,
+                          dstr16 * 16u, full + s);
         }
         __syncwarp();
         if (++ch == nch) {
@@ -791,8 +823,8 @@ __global__ void __maxnreg__(128)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB, dstr16);
-          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB, dstr16);
+          if (q > 0) issue_stage<MB, KS, S::LV, NC, false>(tmem, dA, dB);
+          else issue_stage<MB, KS, S::LV, NC, true>(tmem, dA, dB);
           mma_commit(empty + s);
         }
         __syncwarp();

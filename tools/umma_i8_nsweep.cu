@@ -28,13 +28,18 @@ __device__ __forceinline__ void wait_bar(unsigned long long* bar, uint32_t ph) {
                "@!P1 bra W_%=;\n\t}\n" ::"r"(su32(bar)), "r"(ph));
 }
 
+__device__ int g_random = 0;  // 1: pseudo-random operand bytes (hash), 0: the (i * 37) ramp
 template <int KS, int NC>
 __global__ void k_pat(int mode, int n, int iters, int copy_bytes, const unsigned char* src, long long* cyc) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ unsigned long long bar, cbar[4];
   __shared__ uint32_t tbase;
   constexpr int A_BYTES = KS * 4096, B_BYTES = KS * NC * 32;
-  for (int i = threadIdx.x; i < A_BYTES + B_BYTES; i += blockDim.x) sm[i] = (unsigned char)(i * 37);
+  for (int i = threadIdx.x; i < A_BYTES + B_BYTES; i += blockDim.x) {
+    unsigned h = (unsigned)i * 2654435761u + blockIdx.x * 40503u;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    sm[i] = g_random ? (unsigned char)(h >> 11) : (unsigned char)(i * 37);
+  }
   unsigned char* ring = sm + ((A_BYTES + B_BYTES + 1023) & ~1023);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
@@ -126,6 +131,38 @@ double run(int mode, int n, int copy_bytes, int sms, const unsigned char* src, l
   return best;
 }
 
+// the stage pattern held for `secs` seconds; rate over the last 20 % (power-limited clocks)
+template <int KS, int NC>
+double run_sustained(double secs, int sms, const unsigned char* src, long long* cyc, int random) {
+  auto kern = k_pat<KS, NC>;
+  const int smem = ((KS * 4096 + KS * NC * 32 + 1023) & ~1023) + 1024;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaMemcpyToSymbol(g_random, &random, sizeof(int));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4000;
+  kern<<<sms, 64, smem>>>(1, 0, iters, 0, src, cyc);
+  cudaEventRecord(e0);
+  kern<<<sms, 64, smem>>>(1, 0, iters, 0, src, cyc);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms1 = 0.f;
+  cudaEventElapsedTime(&ms1, e0, e1);
+  const int warm = (int)(secs * 800.0 / ms1), meas = (int)(secs * 200.0 / ms1) + 1;
+  for (int i = 0; i < warm; ++i) kern<<<sms, 64, smem>>>(1, 0, iters, 0, src, cyc);
+  cudaEventRecord(e0);
+  for (int i = 0; i < meas; ++i) kern<<<sms, 64, smem>>>(1, 0, iters, 0, src, cyc);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  int zero = 0;
+  cudaMemcpyToSymbol(g_random, &zero, sizeof(int));
+  const double cols = (double)KS * (KS + 1) / 2 * NC;
+  return 2.0 * 128 * cols * 32 * iters * sms * meas / (ms * 1e-3) / 1e12;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -156,6 +193,10 @@ int main() {
     const double stage_us = ms * 1e3 / 4000;
     printf("{\"mode\": \"stage 7x64 + %d KB bulk copy per stage\", \"tops\": %.1f, \"stage_us\": %.3f, \"copy_TBs\": %.2f}\n",
            kb, t, stage_us, kb * 1024.0 * sms / (stage_us * 1e-6) / 1e12);
+  }
+  for (int rnd : {0, 1}) {
+    const double t = run_sustained<6, 64>(4.0, sms, src, cyc, rnd);
+    printf("{\"mode\": \"stage 6x64 held 4 s, %s operands\", \"tops_sustained\": %.1f}\n", rnd ? "pseudo-random" : "ramp", t);
   }
   return 0;
 }
