@@ -199,11 +199,12 @@ def run_reference(args, c, rank, world):
     ref = CpuReference(c, tg, sr, args.steps, groups_per_sample=args.ref_groups)
     for _ in range(args.warmup):  # warm-up: the upward pass only (no target leaves)
         ref.op.apply_sampled(q, np.zeros(0, dtype=np.int64))
-    steps = []
+    steps, walls = [], []
     r = None
     for i in range(args.steps):
         r = ref.run(q, i, n_sc)
         steps.append(r["apply_s_extrapolated"])
+        walls.append(r["wall_s"])
     t = float(np.mean(steps))
     value = (c.nt + c.ns) / t
     out = {
@@ -215,6 +216,9 @@ def run_reference(args, c, rank, world):
                          "sample": ref.describe(r, args.steps) + f"; mean over {args.steps} samples (extrapolated)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "setup_s": ref.setup_s,
+        # ms_per_step is the full apply EXTRAPOLATED from the step's bounded sample; the wall
+        # time a step actually took on the host is this:
+        "extrapolated": True, "sample_wall_ms_per_step": 1e3 * float(np.mean(walls)),
     }
     print(json.dumps(out), flush=True)
 
