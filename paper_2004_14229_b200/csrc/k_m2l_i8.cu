@@ -249,12 +249,17 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
     __syncthreads();
   }
   double mx = 0.0;
-  for (int idx = threadIdx.x; idx < kCplRows * n; idx += blockDim.x) {
-    const int j = r0 + idx / n, k = idx % n;
-    if (j >= n) continue;
-    const double d[3] = {__dsub_rn(tn[0][j / (p * p)], sn[0][k / (p * p)]),
-                         __dsub_rn(tn[1][(j / p) % p], sn[1][(k / p) % p]),
-                         __dsub_rn(tn[2][j % p], sn[2][k % p])};
+  // work unit = (source node k, half of the CTA's 8 target rows): the source coordinates
+  // stay in registers over 4 rows -- no per-entry index divisions
+  const int pp = p * p;
+  for (int u = threadIdx.x; u < 2 * n; u += blockDim.x) {
+   const int half = u >= n ? 1 : 0, k = u - half * n;
+   const double s0 = sn[0][k / pp], s1 = sn[1][(k / p) % p], s2 = sn[2][k % p];
+   for (int jr = 4 * half; jr < 4 * half + 4; ++jr) {
+    const int j = r0 + jr;
+    if (j >= n) break;
+    const double d[3] = {__dsub_rn(tn[0][j / pp], s0), __dsub_rn(tn[1][(j / p) % p], s1),
+                         __dsub_rn(tn[2][j % p], s2)};
     const double r = sqrt(dot3(d, d));  // geometry.hpp:92-98
     const double ph = __dmul_rn(kappa, __dsub_rn(r, dot3(d, cv)));
     const double w = __ddiv_rn(1.0, __dmul_rn(kFourPi, r));
@@ -278,6 +283,7 @@ __global__ void __launch_bounds__(256) k_coupling_i8(const Consts* __restrict__ 
 #pragma unroll
       for (int i = 0; i < KS; ++i) sb[i * nch * 256] = h ? di[i] : dr[i];
     }
+   }
   }
   if (pass) {
     // M-block b belongs to group g = b / gs (gs = 2: blocks {0, 1}, {2}; gs = 1: one
@@ -1107,11 +1113,10 @@ void launch_coupling_i8(cudaStream_t st, const Consts* C, const double* dirtab, 
   if (nkeys <= 0) return;
   dim3 grid((unsigned)nkeys, (unsigned)((n + kCplRows - 1) / kCplRows));
   const size_t sm = pass ? (size_t)kI8Digits * (2 * nkq / kKC) * 256 : 0;
-  static size_t sm_set = 0;
-  if (sm > 40 * 1024 && sm > sm_set) {  // static shared (node tables) counts towards the 48 KB default
+  // static shared (node tables) counts towards the 48 KB default; the attribute is per
+  // device (n_gpus > 1), so it is set on every launch that needs it
+  if (sm > 40 * 1024)
     cudaFuncSetAttribute(k_coupling_i8<kI8Digits>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    sm_set = sm;
-  }
   k_coupling_i8<kI8Digits><<<grid, 256, sm, st>>>(C, dirtab, key0, key_level, key_d, key_dir, pass, lvmax, Wq, n, nkq,
                                                   (n + 127) / 128, gs, key_base);
 }
