@@ -500,3 +500,28 @@ def test_m2l_hybrid_mode(m, monkeypatch):
     op2 = F.DirectionalOperator(*args)
     assert op2.stats()["w_segments"] >= 3
     assert np.array_equal(op2.apply(q), y)
+
+
+@pytest.mark.parametrize("m", [4, 6])
+def test_int8_m2l_wide_dynamic_range(m):
+    """The int8 M2L rounds moments against one scale per level: charges spanning twelve
+    orders of magnitude, clustered sources (box populations from 1 to hundreds) and a
+    zero block of charges must still give y within 1e-12 (relative l2) of the oracle --
+    the absolute rounding error is relative to the level's largest moment, as the
+    l2 norm of y is."""
+    rng = np.random.default_rng(900 + m)
+    nt, ns = 9000, 8000
+    tg = [rng.random(nt) for _ in range(3)]
+    ctr = rng.random((6, 3))
+    sr = [np.clip(ctr[rng.integers(0, 6, ns), a] + 0.04 * rng.standard_normal(ns), 1e-9, 1.0) for a in range(3)]
+    mag = 10.0 ** rng.uniform(-6, 6, ns)
+    q = mag * np.exp(2j * np.pi * rng.random(ns))
+    q[: ns // 10] = 0.0
+    y, yo, op, _ = run_pair(tg, sr, q, (0, 0, 0), (1, 1, 1), 14.0, 32, m, 1.0, -2)
+    assert op.stats()["m2l_impl"] == 1 and op.stats()["n_c"] > 0
+    err = oracle.rel_l2(y, yo)
+    print(f"m={m}: wide dynamic range, rel l2 vs oracle {err:.2e}")
+    assert err <= TOL
+    # all-zero charges: zero moments (scale exponent of 0) -> exactly zero far field
+    y0 = op.apply(np.zeros(ns, dtype=np.complex128))
+    assert np.all(y0 == 0)
