@@ -51,9 +51,6 @@
 #ifndef FDH_I8P_G
 #define FDH_I8P_G 1  // k_m2l_i8p: moment-gather stages in flight per warp (beyond the one being issued)
 #endif
-#ifndef FDH_I8_PAIR2_DEFAULT
-#define FDH_I8_PAIR2_DEFAULT 0  // 1: pair items run k_m2l_i8pp (halves, two TMEM accumulator sets)
-#endif
 #ifndef FDH_I8_EXP
 #define FDH_I8_EXP 0  // timing experiments: 1 = no B gather, 2 = no W copy, 3 = neither (wrong results)
 #endif
@@ -1063,275 +1060,6 @@ void run_i8p(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass
                                             pass * a.n_tile, a.key_base, a.nrhs, a.pair_out, w.wkc, w.wst, w.dstr16);
 }
 
-// ---------------------------------------------------------------- M2L, pair items, two accumulator sets
-// Pair items are one key long (nch stages), so in k_m2l_i8p the TMEM epilogue of an
-// item is exposed: the next item's first MMA waits for it (rate ~0.7 of the target
-// tiles).  Here a 32-pair item runs as two halves of 16 pairs, each with its own TMEM
-// accumulator set (LV x 32 columns at column 0 / 256): the epilogue of one half
-// overlaps the MMAs of the next half or item.  Cost: W is streamed once per half.
-// Pair tiles (append_pair_part) have identity column maps: pair c of the tile is
-// column c, its source slot tile_src[row * 32 + c].  One rhs.
-template <int KS, int NST, int NGW>
-__global__ void __maxnreg__(128)
-    k_m2l_i8pp(const int32_t* __restrict__ item_tile, const int64_t* __restrict__ item_k0,
-               const int32_t* __restrict__ tile_level, const int32_t* __restrict__ tile_keys,
-               const int32_t* __restrict__ tile_src, const uint8_t* __restrict__ tile_cnt,
-               const int8_t* __restrict__ Wq, const int8_t* __restrict__ Mq,
-               const unsigned long long* __restrict__ lvmax_w, const unsigned long long* __restrict__ lvmax_v,
-               int* __restrict__ counter, int item0, int n_item, int nkq, int n_pad, int blk0, int64_t key_base,
-               double* __restrict__ pair_out, int wkc, int wst_bytes, uint32_t dstr16) {
-  constexpr int TTA = 32;  // pairs per tile (row stride of the tile arrays)
-  constexpr int TH = 16;   // pairs per half
-  using S = I8Shape<1, TH, KS, NST, NGW>;
-  constexpr int NC = S::NC;  // 32 real columns per digit block
-  constexpr int EW0 = 2 + NGW;
-  constexpr int SETC = 256;  // TMEM column offset of the second accumulator set
-  static_assert(S::LV * NC <= SETC, "accumulator set");
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* wst = smem;
-  uint8_t* bst = smem + NST * S::WST;
-  uint64_t* full = reinterpret_cast<uint64_t*>(bst + NST * S::BST);
-  uint64_t* fullb = full + NST;
-  uint64_t* empty = fullb + NST;
-  uint64_t* meta_full = empty + NST;     // [2]
-  uint64_t* meta_empty = meta_full + 2;  // [2]
-  uint64_t* tmem_full = meta_empty + 2;  // [2]: one per accumulator set
-  uint64_t* tfree = tmem_full + 2;       // [2]
-  uint32_t* tbase_s = reinterpret_cast<uint32_t*>(tfree + 2);
-  __shared__ int s_idx[2];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nch = 2 * nkq / kKC;
-  for (int i = tid * 16; i < NST * S::WST; i += (int)blockDim.x * 16) *reinterpret_cast<int4*>(wst + i) = make_int4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (tid == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(fullb + s, NGW);
-      mbar_init(empty + s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(meta_full + b, 1);
-      mbar_init(meta_empty + b, NGW + 1 + 4);
-      mbar_init(tmem_full + b, 1);
-      mbar_init(tfree + b, 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase_s)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tbase_s;
-
-  if (warp == 0) {
-    // ---------------- producer: claims + W stream (once per half)
-    uint32_t qbase = 0;
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      if (it >= 2) mbar_wait_sleep(meta_empty + b, ((it - 2) >> 1) & 1);
-      int idx = 0;
-      if (lane == 0) {
-        idx = atomicAdd(counter, 1);
-        s_idx[b] = idx;
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_full + b)) : "memory");
-      }
-      idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (idx >= n_item) break;
-      const int64_t k0 = item_k0[item0 + idx];
-      const int key = tile_keys[k0];
-      const int Q = (tile_cnt[k0] > TH ? 2 : 1) * nch;
-      int ch = 0;
-      for (int q = 0; q < Q; ++q) {
-        const uint32_t qg = qbase + q;
-        const int s = qg % NST;
-        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
-        if (lane == 0)
-          w_stage_g2s<KS>(wst + s * S::WST, Wq + (((int64_t)key - key_base) * nch + ch) * (int64_t)wkc + blk0 * (KS * kCore),
-                          wst_bytes, dstr16 * 16u, full + s);
-        __syncwarp();
-        if (++ch == nch) ch = 0;
-      }
-      qbase += (uint32_t)Q;
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
-    const uint64_t dA0 = sdesc(smem_u32(wst)), dB0 = sdesc(smem_u32(bst));
-    uint32_t qbase = 0, vit = 0;
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      mbar_wait(meta_full + b, (it >> 1) & 1);
-      const int idx = s_idx[b];
-      if (idx >= n_item) break;
-      const int nh = tile_cnt[item_k0[item0 + idx]] > TH ? 2 : 1;
-      for (int h = 0; h < nh; ++h, ++vit) {
-        const uint32_t set = vit & 1;
-        if (vit >= 2) mbar_wait(tfree + set, ((vit >> 1) - 1) & 1);  // the epilogue has read this set
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int q = 0; q < nch; ++q) {
-          const uint32_t qg = qbase + q;
-          const int s = qg % NST;
-          const uint32_t ph = (qg / NST) & 1;
-          mbar_wait(full + s, ph);
-          mbar_wait(fullb + s, ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (lane == 0) {
-            const uint64_t dA = dA0 + (uint64_t)((s * S::WST) >> 4), dB = dB0 + (uint64_t)((s * S::BST) >> 4);
-            if (q > 0) issue_stage<1, KS, S::LV, NC, false>(tmem + set * SETC, dA, dB);
-            else issue_stage<1, KS, S::LV, NC, true>(tmem + set * SETC, dA, dB);
-            mma_commit(empty + s);
-          }
-          __syncwarp();
-        }
-        if (lane == 0) mma_commit(tmem_full + set);
-        __syncwarp();
-        qbase += (uint32_t)nch;
-      }
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
-      __syncwarp();
-    }
-  } else if (warp < EW0) {
-    // ---------------- gather (16 columns per stage)
-    constexpr int RND = (KS * 4 + 7) / 8;
-    constexpr int U = (TH / 4) * RND;
-    constexpr int UPW = (U + NGW - 1) / NGW;
-    constexpr int G = 1;
-    int dsto[UPW], gofs[UPW], ccol[UPW];
-    {
-      const int cl = lane >> 3, p8 = lane & 7;
-#pragma unroll
-      for (int t = 0; t < UPW; ++t) {
-        const int u = (warp - 2) + t * NGW;
-        const int cg = u / RND, r = u % RND;
-        const int pc = 8 * r + p8;
-        const int c = 4 * cg + cl;
-        const bool ok = u < U && pc < KS * 4;
-        const int hh = pc & 1, kb = (pc >> 1) & 1, j = pc >> 2;
-        const int n = j * NC + 2 * c + hh;
-        dsto[t] = ok ? ((n >> 3) * 2 + kb) * 128 + (n & 7) * 16 : -1;
-        gofs[t] = pc * 16;
-        ccol[t] = ok ? c : 0;
-      }
-    }
-    auto arrive = [&](uint32_t qa) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(fullb + qa % NST)) : "memory");
-    };
-    uint32_t qbase = 0;
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      mbar_wait_sleep(meta_full + b, (it >> 1) & 1);
-      const int idx = s_idx[b];
-      if (idx >= n_item) break;
-      const int64_t k0 = item_k0[item0 + idx];
-      const int cnt = tile_cnt[k0];
-      const int Q = (cnt > TH ? 2 : 1) * nch;
-      const int srcl = lane < cnt ? tile_src[k0 * TTA + lane] : -1;  // source slot of pair `lane`
-      int srcv[UPW];
-#pragma unroll
-      for (int t = 0; t < UPW; ++t) srcv[t] = __shfl_sync(0xffffffffu, srcl, ccol[t]);
-      int ch = 0;
-      for (int q = 0; q < Q; ++q) {
-        const uint32_t qg = qbase + q;
-        const int s = qg % NST;
-        if (qg >= NST) mbar_wait_sleep(empty + s, ((qg / NST) - 1) & 1);
-        uint8_t* bb = bst + s * S::BST;
-        const int8_t* mq = Mq + (int64_t)ch * (KS * 64);
-#pragma unroll
-        for (int t = 0; t < UPW; ++t) {
-          if (dsto[t] < 0) continue;
-          if (srcv[t] >= 0) cp_async16(bb + dsto[t], mq + (int64_t)srcv[t] * nch * (KS * 64) + gofs[t]);
-          else *reinterpret_cast<int4*>(bb + dsto[t]) = make_int4(0, 0, 0, 0);
-        }
-        cp_async_commit();
-        if (q >= G) {
-          cp_async_wait<G>();
-          arrive(qg - G);
-        }
-        if (++ch == nch) {  // second half: pairs 16 .. 31
-          ch = 0;
-#pragma unroll
-          for (int t = 0; t < UPW; ++t) srcv[t] = __shfl_sync(0xffffffffu, srcl, TH + ccol[t]);
-        }
-      }
-      cp_async_wait<0>();
-      for (int qa = Q > G ? Q - G : 0; qa < Q; ++qa) arrive(qbase + qa);
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
-      qbase += (uint32_t)Q;
-    }
-  } else {
-    // ---------------- epilogue (4 warps, TMEM lane quarter = warp & 3)
-    const int qw = warp & 3;
-    double fL[S::LV];
-#pragma unroll
-    for (int L = 0; L < S::LV; ++L) fL[L] = ldexp(1.0, -kI8Bits * (L + 2));
-    uint32_t vit = 0;
-    for (int it = 0;; ++it) {
-      const int b = it & 1;
-      mbar_wait_sleep(meta_full + b, (it >> 1) & 1);
-      const int idx = s_idx[b];
-      if (idx >= n_item) break;
-      const int item = item0 + idx;
-      const int nh = tile_cnt[item_k0[item]] > TH ? 2 : 1;
-      const int lvl = tile_level[item_tile[item]];
-      const double sc = ldexp(1.0, level_exp(lvmax_w, lvl) + 2 + level_exp(lvmax_v, lvl));
-      const int row = blk0 * 128 + qw * 32 + lane;
-      for (int h = 0; h < nh; ++h, ++vit) {
-        const uint32_t set = vit & 1;
-        mbar_wait_sleep(tmem_full + set, (vit >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-        for (int g = 0; g < NC / 8; ++g) {
-          uint32_t r[S::LV][8];
-#pragma unroll
-          for (int L = 0; L < S::LV; ++L)
-            tmem_ld8(tmem + ((uint32_t)(qw * 32) << 16) + set * SETC + L * NC + 8 * g, r[L]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (row >= n_pad) continue;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            double a = 0.0;
-#pragma unroll
-            for (int L = S::LV - 1; L >= 0; --L) a += i32_to_f64(r[L][e]) * fL[L];
-            const int col = 8 * g + e;
-            pair_out[((int64_t)idx * TTA + TH * h + (col >> 1)) * 2 * n_pad + (col & 1) * n_pad + row] = a * sc;
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == EW0 && lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tfree + set)) : "memory");
-      }
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(meta_empty + b)) : "memory");
-    }
-  }
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-template <int NST, int NGW>
-void run_i8pp(cudaStream_t st, const M2LI8Args& a, int mb_tot, int blk0, int pass) {
-  using S = I8Shape<1, 16, kI8Digits, NST, NGW>;
-  const WPass w = wpass<1>(a, mb_tot, blk0, true);
-  auto kern = k_m2l_i8pp<kI8Digits, NST, NGW>;
-  const size_t sm = (size_t)NST * S::STAGE + (3 * NST + 8) * 8 + 16;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::max(1, std::min(a.n_item, nsm));
-  kern<<<grid, (2 + NGW + 4) * 32, sm, st>>>(a.item_tile, a.item_k0, a.tile_level, a.tile_keys, a.tile_src, a.tile_cnt, a.Wq,
-                                             a.Mq, a.lvmax_w, a.lvmax_v, a.counter + pass, a.item0, a.n_item, a.nkq,
-                                             a.n_pad, blk0, a.key_base, a.pair_out, w.wkc, w.wst, w.dstr16);
-}
-
 template <int MB, int TT, int NST, int NGW>
 size_t i8_smem(int fkeys) {
   using S = I8Shape<MB, TT, kI8Digits, NST, NGW>;
@@ -1426,14 +1154,6 @@ int launch_m2l_i8(cudaStream_t st, int n, int tile, const M2LI8Args& a) {
   // passes over the item list (m2l_i8_passes): one per M-block group; a.counter
   // holds one zeroed claim counter per pass (and per segment)
   constexpr int kResP = 4096;  // barriers + static shared + alignment (k_m2l_i8p)
-  // pair items of 32-wide plans (one rhs): two halves with their own TMEM accumulator
-  // sets, the epilogue overlapped (k_m2l_i8pp); FDH_I8_PAIR2=0 keeps k_m2l_i8p
-  const char* p2e = std::getenv("FDH_I8_PAIR2");  // read per launch (graph capture): A/B inside one process
-  const bool pair2 = p2e ? p2e[0] == '1' : FDH_I8_PAIR2_DEFAULT != 0;
-  if (a.pair_out && tile == 32 && a.nrhs == 1 && pair2 && m2l_i8_wgroup_of(mb, 32) == 1) {
-    for (int b = 0; b < mb; ++b) run_i8pp<nst_fit(1, 16, kResP), 8>(st, a, mb, b, b);
-    return 0;
-  }
   if (pipe) {
     if (mb == 1 && tile == 32) {
       run_i8p<1, 32, nst_fit(1, 32, kResP), 8>(st, a, 1, 0, 0);
