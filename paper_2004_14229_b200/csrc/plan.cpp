@@ -924,8 +924,15 @@ void build_m2l(Plan& P) {
   // int8: 48 MB (profiles/r02_m2l_sweep_tt_chunk.jsonl: 2-3 % faster than 24 MB on configs 3, 5
   // and the m = 6 shape); DMMA: optimum 8-12 MB (profiles/r01_m2l_chunk_sweep.txt)
   int64_t chunk_mb = P.prm.m2l_impl == 1 ? 48 : 12;
-  if (const char* e = std::getenv("FDH_M2L_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));  // tuning knob
-  const int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
+  const char* cme = std::getenv("FDH_M2L_CHUNK_MB");  // tuning knob
+  if (cme) chunk_mb = std::max(1L, std::atol(cme));
+  int64_t cw = std::max<int64_t>(16, (chunk_mb << 20) / wbytes);
+  // int8: a chunk wider than the exact-int32 key bound F splits every (tile, chunk) into
+  // items of F and (chunk - F) keys; one item per (tile, chunk) measured 11 % faster at
+  // m = 5 (chunk 73 -> 48 keys: config 3 M2L 1317 -> 1168 ms) and 6 % at m = 4 (256 -> 85
+  // keys: config 2 23.5 -> 22.2 ms); m = 6 has 31 = F keys per 48 MB chunk already
+  // (profiles/r02_m2l_chunk_vs_fkeys.jsonl)
+  if (!cme && P.prm.m2l_impl == 1 && P.prm.m2l_fkeys > 0) cw = std::min<int64_t>(cw, P.prm.m2l_fkeys);
   P.m2l_chunk = cw;
   std::vector<std::array<int64_t, 4>> items;  // chunk, tile, k0, k1
   const int64_t fk = P.prm.m2l_fkeys > 0 ? P.prm.m2l_fkeys : INT64_MAX;  // k_m2l_i8: exact int32 sums
